@@ -1,0 +1,164 @@
+/* mf.h -- C ABI of the B200-native Matrix Flow hot path (libmf.so).
+ *
+ * The method (arXiv 2312.12732, PAPER.md): C = alpha * A * B for square
+ * n x n double-precision matrices, computed by
+ * a bilinear factorization <U,V,W> -- the paper's a, b, c (PAPER.md
+ * L196-220, Eq. "strassen"):
+ *
+ *     C_i = sum_q W[i][q] * P_q,   P_q = T_q * S_q,
+ *     T_q = sum_k U[k][q] * A_k,   S_q = sum_l V[l][q] * B_l,
+ *
+ * over the p-way row-major block partition of A, B, C (PAPER.md L134-165,
+ * L208-211), applied recursively `levels` times.  The
+ * `levels` recursion is executed as ONE level of the Kronecker-flattened
+ * triple U^(x)L, V^(x)L, W^(x)L, the bilinear map the
+ * recursion computes.
+ *
+ * Conventions shared by every entry point:
+ *  - Matrices are row-major fp64 with a leading dimension in ELEMENTS
+ *    (ld >= n).  Device pointers unless a function says "host".
+ *  - Coefficient arrays are HOST arrays of p*p x R doubles, row-major:
+ *    U[k*R+q] = a_{k,q}, V[l*R+q] = b_{l,q}, W[i*R+q] = c_{i,q} with row i
+ *    the C block in natural row-major order (PAPER.md prints c^t with rows
+ *    C0, C2, C1, C3 -- L245-248; callers importing that layout must reorder).
+ *  - Every function returns mf_status; no C++ exception crosses the ABI.
+ *    On a non-OK status, mf_last_error() returns a thread-local message.
+ *  - Work is stream-ordered and asynchronous on the given cudaStream_t
+ *    (passed as void*, NULL = legacy default stream) unless stated.
+ */
+#ifndef MF_H
+#define MF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MF_OK = 0,
+  MF_ERR_INVALID_ARG = 1,   /* null/negative/overlapping/misaligned argument     */
+  MF_ERR_INDIVISIBLE = 2,   /* n % p^levels != 0 (no padding: PAPER.md L487-488) */
+  MF_ERR_BAD_TRIPLE = 3,    /* Brent equations violated or a dead product column */
+  MF_ERR_OUT_OF_MEMORY = 4, /* device or host allocation failed                  */
+  MF_ERR_CUDA = 5,          /* a CUDA runtime/driver call failed                 */
+  MF_ERR_NCCL = 6,          /* an NCCL call failed                               */
+  MF_ERR_UNSUPPORTED = 7    /* valid request outside what this build implements  */
+} mf_status;
+
+typedef struct mf_plan_st* mf_plan_t;
+
+enum { MF_LEAF_DMMA = 0, MF_LEAF_SIMPLE = 1 };
+enum { MF_IN_ROOT = 0, MF_IN_REPLICATED = 1 };
+enum { MF_OUT_ROOT = 0, MF_OUT_ALL = 1 };
+
+typedef struct {
+  int32_t struct_size;  /* sizeof(mf_options); 0-initialised struct = defaults    */
+  int32_t device;       /* CUDA device ordinal; -1 = current device (default)     */
+  int32_t leaf;         /* MF_LEAF_DMMA (default): TMA + mma.sync f64 leaf GEMM;
+                           MF_LEAF_SIMPLE: plain fp64 FMA leaf (test ablation)    */
+  int32_t shard_rank;   /* product sharding: this rank's index (default 0)        */
+  int32_t shard_count;  /* number of shards; 0/1 = unsharded.  With nccl_comm ==
+                           NULL a sharded plan computes only its shard's PARTIAL C
+                           (used to emulate rank r of N on one GPU)               */
+  void* nccl_comm;      /* ncclComm_t from mf_nccl_comm_create, or NULL           */
+  int32_t input_mode;   /* MF_IN_REPLICATED (inputs valid on every rank) or
+                           MF_IN_ROOT (rank 0's A, B are broadcast first)         */
+  int32_t output_mode;  /* MF_OUT_ROOT (C summed onto rank 0) or MF_OUT_ALL
+                           (C summed onto every rank)                             */
+} mf_options;
+
+/* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.
+ * Host-side and untimed:
+ *  1. checks p >= 1, R >= 1, levels >= 0, n >= 1 (MF_ERR_INVALID_ARG);
+ *  2. checks the Brent equations exactly over all (p^2)^3 index triples
+ *      and that no U/V column is zero (MF_ERR_BAD_TRIPLE;
+ *     coefficients must be integers or dyadic rationals, else
+ *     MF_ERR_UNSUPPORTED);
+ *  3. checks n % p^levels == 0 (MF_ERR_INDIVISIBLE, message names n, p, L);
+ *  4. Kronecker-flattens the triple `levels` times (SPEC.md L244 interleave,
+ *     product index q = q_outer * R + q_inner);
+ *  5. classifies operand columns: a column with a single +-1 entry aliases its
+ *     A/B block (sign folded into W), others are materialised by the
+ *     pre-addition kernel;
+ *  6. allocates the device workspace (T, S, P blocks) and TMA descriptors.
+ * levels == 0 plans a classical C = alpha*A*B on the leaf kernel (U,V,W may
+ * then be NULL).  The plan owns its workspace; the caller owns A, B, C.
+ * A plan is bound to one device.  *out is NULL on failure. */
+mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const double* V,
+                  const double* W, int32_t levels, int64_t n, const mf_options* opt);
+
+/* mf_dgemm -- C <- alpha * A * B through the planned algorithm.
+ * A (n x n, lda), B (n x n, ldb): device, read-only.  C (n x n, ldc): device,
+ * write-only (BLAS beta = 0: prior contents, even NaN, are ignored); C must
+ * not overlap A or B (MF_ERR_INVALID_ARG).  Launches, in stream order:
+ * pre-add A (K4), pre-add B (K4), the batched leaf DGEMM (K5), post-add
+ * (K6) -- no host synchronisation.  Calls on one plan must be serialised by
+ * the caller (they share the workspace).  Inputs must be finite: the fast
+ * algorithm turns Inf-Inf into NaN where the classical product gives +-Inf.
+ * With a sharded plan (shard_count > 1) and no NCCL communicator, C receives
+ * this shard's PARTIAL sum (the W-combination over the shard's products). */
+mf_status mf_dgemm(mf_plan_t plan, double alpha, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* mf_dgemm_host -- the same product with HOST A, B, C (any host memory;
+ * pinned memory is fastest).  Copies A and B to plan-owned device buffers,
+ * runs mf_dgemm, copies C back; returns after C is complete on the host. */
+mf_status mf_dgemm_host(mf_plan_t plan, double alpha, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* mf_destroy -- wait for the plan's outstanding work, free it.  NULL: no-op. */
+mf_status mf_destroy(mf_plan_t plan);
+
+/* Thread-local message for the last non-OK status of this thread ("" if none). */
+const char* mf_last_error(void);
+
+/* Plan facts: workspace bytes, leaf side m = n / p^levels, number of leaf
+ * products R^levels, materialised T / S counts.  Any pointer may be NULL. */
+mf_status mf_plan_info(mf_plan_t plan, size_t* workspace_bytes, int64_t* leaf_n,
+                       int64_t* n_products, int32_t* n_mat_a, int32_t* n_mat_b);
+
+/* Per-product routing of the flattened triple, arrays of length n_products
+ * (host, caller-allocated, any may be NULL): a_src[q] = 0 if P_q's left
+ * operand aliases block a_idx[q] of A, 1 if it is materialised slot a_idx[q]
+ * of the T workspace; b_src/b_idx likewise for B and S; sign[q] = +-1, the
+ * sign folded out of aliased operands (P_q as produced by the leaf stage is
+ * sign[q] times the P_q of Eq. "strassen"); shard[q] = the shard that computes
+ * product q. */
+mf_status mf_plan_products(mf_plan_t plan, int32_t* a_src, int32_t* a_idx, int32_t* b_src,
+                           int32_t* b_idx, int32_t* sign, int32_t* shard);
+
+/* Component entry points (the steps of mf_dgemm, exposed for step-by-step
+ * parity tests against the oracle; stream-ordered, device pointers):
+ *  mf_premix:  side 0: T slots from A, side 1: S slots from B.  out holds
+ *              n_mat_{a,b} x m x m doubles; slot s = the s-th materialised
+ *              column in ascending q (K4).
+ *  mf_leaf:    P_q' = T_q * S_q for this plan's products (K5); A, B are the
+ *              operands that alias, T, S the materialised slots (as mf_premix
+ *              writes them), P holds n_products x m x m doubles.
+ *  mf_postmix: C_i = alpha * sum_q (W[i][q]*sign[q]) * P_q' (K6), P as mf_leaf
+ *              writes it. */
+mf_status mf_premix(mf_plan_t plan, int32_t side, const double* X, int64_t ldx, double* out,
+                    void* stream);
+mf_status mf_leaf(mf_plan_t plan, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  const double* T, const double* S, double* P, void* stream);
+mf_status mf_postmix(mf_plan_t plan, double alpha, const double* P, double* C, int64_t ldc,
+                     void* stream);
+
+/* Multi-GPU bootstrap (NCCL over NVLink; the 128-byte unique id is exchanged
+ * by the caller, e.g. through torch.distributed).  Each rank then passes the
+ * communicator in mf_options.nccl_comm with shard_rank = rank and
+ * shard_count = nranks; mf_dgemm computes the rank's products and sums the
+ * partial C with ncclReduce (MF_OUT_ROOT) or ncclAllReduce (MF_OUT_ALL). */
+mf_status mf_nccl_unique_id(void* id_out /* 128 bytes */);
+mf_status mf_nccl_comm_create(void** comm_out, const void* id, int32_t rank, int32_t nranks);
+mf_status mf_nccl_comm_destroy(void* comm);
+
+/* Library version, e.g. "mf 0.1.0 sm_100a". */
+const char* mf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MF_H */

@@ -1,0 +1,263 @@
+"""B200-native Matrix Flow hot path (arXiv 2312.12732): Python binding of libmf.so.
+
+Argument marshalling only: every step of the path (pre-additions K4, batched
+leaf DGEMM K5, post-addition K6, NCCL reduction) runs inside libmf.so.  The C
+ABI is include/mf.h; the names here mirror it.  PyTorch supplies device
+memory, streams and process groups.  There is no fallback: if libmf.so is
+missing this import fails.
+
+    import torch, paper_2312_12732_b200 as mf
+    plan = mf.Plan(mf.triples.STRASSEN_WINOGRAD, levels=2, n=16384)
+    C = plan.dgemm(A, B)              # A, B: cuda float64, row-major
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import triples
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmf.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python tools/build_mf.py` "
+                      "(the CUDA path has no fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+MF_OK, MF_ERR_INVALID_ARG, MF_ERR_INDIVISIBLE, MF_ERR_BAD_TRIPLE = 0, 1, 2, 3
+MF_ERR_OUT_OF_MEMORY, MF_ERR_CUDA, MF_ERR_NCCL, MF_ERR_UNSUPPORTED = 4, 5, 6, 7
+STATUS_NAMES = {0: "MF_OK", 1: "MF_ERR_INVALID_ARG", 2: "MF_ERR_INDIVISIBLE",
+                3: "MF_ERR_BAD_TRIPLE", 4: "MF_ERR_OUT_OF_MEMORY", 5: "MF_ERR_CUDA",
+                6: "MF_ERR_NCCL", 7: "MF_ERR_UNSUPPORTED"}
+LEAF_DMMA, LEAF_SIMPLE = 0, 1
+IN_ROOT, IN_REPLICATED = 0, 1
+OUT_ROOT, OUT_ALL = 0, 1
+
+EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
+           "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
+           "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version")
+
+
+class mf_options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("leaf", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
+                ("shard_count", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
+                ("input_mode", ctypes.c_int32), ("output_mode", ctypes.c_int32)]
+
+
+_P, _D, _I32, _I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64
+_lib.mf_plan.argtypes = [ctypes.POINTER(_P), _I32, _I32, _P, _P, _P, _I32, _I64,
+                         ctypes.POINTER(mf_options)]
+_lib.mf_dgemm.argtypes = [_P, _D, _P, _I64, _P, _I64, _P, _I64, _P]
+_lib.mf_dgemm_host.argtypes = [_P, _D, _P, _I64, _P, _I64, _P, _I64, _P]
+_lib.mf_destroy.argtypes = [_P]
+_lib.mf_last_error.argtypes = []
+_lib.mf_last_error.restype = ctypes.c_char_p
+_lib.mf_version.restype = ctypes.c_char_p
+_lib.mf_plan_info.argtypes = [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_I64),
+                              ctypes.POINTER(_I64), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
+_lib.mf_plan_products.argtypes = [_P] * 7
+_lib.mf_premix.argtypes = [_P, _I32, _P, _I64, _P, _P]
+_lib.mf_leaf.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _P, _P]
+_lib.mf_postmix.argtypes = [_P, _D, _P, _P, _I64, _P]
+_lib.mf_nccl_unique_id.argtypes = [_P]
+_lib.mf_nccl_comm_create.argtypes = [ctypes.POINTER(_P), _P, _I32, _I32]
+_lib.mf_nccl_comm_destroy.argtypes = [_P]
+for _f in EXPORTS:
+    if _f not in ("mf_last_error", "mf_version"):
+        getattr(_lib, _f).restype = ctypes.c_int
+
+
+class MfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(status: int):
+    if status != MF_OK:
+        raise MfError(status, _lib.mf_last_error().decode())
+
+
+def version() -> str:
+    return _lib.mf_version().decode()
+
+
+def _mat(X, n, name):
+    """(pointer, leading dimension) of a row-major n x n float64 CUDA tensor view."""
+    import torch
+    if not isinstance(X, torch.Tensor) or not X.is_cuda or X.dtype != torch.float64:
+        raise TypeError(f"{name} must be a CUDA float64 tensor")
+    if X.dim() != 2 or tuple(X.shape) != (n, n) or X.stride(1) != 1:
+        raise ValueError(f"{name} must be an n x n row-major view (n={n}), got "
+                         f"shape {tuple(X.shape)} strides {X.stride()}")
+    return X.data_ptr(), X.stride(0)
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """mf_plan / mf_dgemm / mf_destroy for one (triple, levels, n, options)."""
+
+    def __init__(self, triple: triples.Triple | None, levels: int, n: int, *, leaf: str = "dmma",
+                 device: int | None = None, shard_rank: int = 0, shard_count: int = 1,
+                 nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT):
+        self.triple, self.levels, self.n = triple, int(levels), int(n)
+        opt = mf_options()
+        opt.struct_size = ctypes.sizeof(mf_options)
+        opt.device = -1 if device is None else int(device)
+        opt.leaf = {"dmma": LEAF_DMMA, "simple": LEAF_SIMPLE}[leaf]
+        opt.shard_rank, opt.shard_count = int(shard_rank), int(shard_count)
+        opt.nccl_comm = nccl_comm.value if isinstance(nccl_comm, ctypes.c_void_p) else nccl_comm
+        opt.input_mode, opt.output_mode = int(input_mode), int(output_mode)
+        self._opt = opt
+        h = ctypes.c_void_p()
+        if triple is None:
+            _check(_lib.mf_plan(ctypes.byref(h), 1, 1, None, None, None, self.levels, self.n,
+                                ctypes.byref(opt)))
+        else:
+            U = np.ascontiguousarray(triple.U, dtype=np.float64)
+            V = np.ascontiguousarray(triple.V, dtype=np.float64)
+            W = np.ascontiguousarray(triple.W, dtype=np.float64)
+            self._keep = (U, V, W)
+            _check(_lib.mf_plan(ctypes.byref(h), int(triple.p), int(U.shape[1]),
+                                U.ctypes.data, V.ctypes.data, W.ctypes.data, self.levels, self.n,
+                                ctypes.byref(opt)))
+        self._h = h
+
+    # -- queries --------------------------------------------------------------
+    def info(self) -> dict:
+        ws, m, nprod, na, nb = ctypes.c_size_t(), _I64(), _I64(), _I32(), _I32()
+        _check(_lib.mf_plan_info(self._h, ctypes.byref(ws), ctypes.byref(m), ctypes.byref(nprod),
+                                 ctypes.byref(na), ctypes.byref(nb)))
+        return {"workspace_bytes": ws.value, "leaf_n": m.value, "n_products": nprod.value,
+                "n_mat_a": na.value, "n_mat_b": nb.value}
+
+    def products(self) -> dict:
+        nprod = self.info()["n_products"]
+        arrs = {k: np.zeros(nprod, dtype=np.int32)
+                for k in ("a_src", "a_idx", "b_src", "b_idx", "sign", "shard")}
+        _check(_lib.mf_plan_products(self._h, *[arrs[k].ctypes.data for k in
+                                                ("a_src", "a_idx", "b_src", "b_idx", "sign", "shard")]))
+        return arrs
+
+    # -- the hot path ------------------------------------------------------------
+    def dgemm(self, A, B, C=None, alpha: float = 1.0, stream=None):
+        """C <- alpha*A*B on the device (stream-ordered, no host sync)."""
+        import torch
+        n = self.n
+        pa, lda = _mat(A, n, "A") if A is not None else (None, n)
+        pb, ldb = _mat(B, n, "B") if B is not None else (None, n)
+        if C is None:
+            dev = A.device if A is not None else torch.device("cuda")
+            C = torch.empty((n, n), dtype=torch.float64, device=dev)
+        pc, ldc = _mat(C, n, "C")
+        _check(_lib.mf_dgemm(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
+                             _stream_ptr(stream)))
+        return C
+
+    def dgemm_host(self, A: np.ndarray, B: np.ndarray, C: np.ndarray | None = None,
+                   alpha: float = 1.0, stream=None) -> np.ndarray:
+        """The same product on HOST float64 row-major arrays (copies inside the call)."""
+        def host(X, name):
+            if X.dtype != np.float64 or X.ndim != 2 or X.shape != (self.n, self.n) or \
+                    X.strides[1] != 8:
+                raise ValueError(f"{name} must be a row-major {self.n}x{self.n} float64 array")
+            return X.ctypes.data, X.strides[0] // 8
+        if C is None:
+            C = np.empty((self.n, self.n))
+        pa, lda = host(A, "A"); pb, ldb = host(B, "B"); pc, ldc = host(C, "C")
+        _check(_lib.mf_dgemm_host(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
+                                  _stream_ptr(stream)))
+        return C
+
+    def dgemm_host_ptr(self, pa: int, lda: int, pb: int, ldb: int, pc: int, ldc: int,
+                       alpha: float = 1.0, stream=None):
+        """mf_dgemm_host on raw host pointers (e.g. pinned torch CPU tensors)."""
+        _check(_lib.mf_dgemm_host(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
+                                  _stream_ptr(stream)))
+
+    # -- the steps, for step-by-step parity tests -------------------------------
+    def premix(self, side: str, X, out, stream=None):
+        import torch
+        px, ldx = _mat(X, self.n, side)
+        if not out.is_contiguous() or out.dtype != torch.float64:
+            raise ValueError("out must be contiguous float64")
+        _check(_lib.mf_premix(self._h, 0 if side == "A" else 1, px, ldx, out.data_ptr(),
+                              _stream_ptr(stream)))
+        return out
+
+    def leaf(self, A, B, T, S, P, stream=None):
+        pa, lda = _mat(A, self.n, "A")
+        pb, ldb = _mat(B, self.n, "B")
+        _check(_lib.mf_leaf(self._h, pa, lda, pb, ldb,
+                            T.data_ptr() if T is not None and T.numel() else None,
+                            S.data_ptr() if S is not None and S.numel() else None,
+                            P.data_ptr(), _stream_ptr(stream)))
+        return P
+
+    def postmix(self, P, C, alpha: float = 1.0, stream=None):
+        pc, ldc = _mat(C, self.n, "C")
+        _check(_lib.mf_postmix(self._h, float(alpha), P.data_ptr(), pc, ldc, _stream_ptr(stream)))
+        return C
+
+    # -- lifetime ------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _check(_lib.mf_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def dgemm(A, B, triple: triples.Triple | str | None = "strassen-winograd", levels: int = 1,
+          alpha: float = 1.0, leaf: str = "dmma"):
+    """One-shot C = alpha*A*B (plans, runs, destroys; the plan owns scratch memory)."""
+    if isinstance(triple, str):
+        triple = triples.get(triple)
+    with Plan(triple, levels if triple is not None else 0, A.shape[0], leaf=leaf) as p:
+        C = p.dgemm(A, B, alpha=alpha)
+        import torch
+        torch.cuda.current_stream().synchronize()
+    return C
+
+
+# -- NCCL bootstrap (mf_nccl_*) --------------------------------------------------
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.mf_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_create(uid: bytes, rank: int, nranks: int) -> ctypes.c_void_p:
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(_lib.mf_nccl_comm_create(ctypes.byref(comm), buf, rank, nranks))
+    return comm
+
+
+def nccl_comm_destroy(comm: ctypes.c_void_p):
+    _check(_lib.mf_nccl_comm_destroy(comm))
+
+
+__all__ = ["Plan", "dgemm", "MfError", "triples", "version", "nccl_unique_id", "nccl_comm_create",
+           "nccl_comm_destroy", "EXPORTS", "LIB_PATH"]

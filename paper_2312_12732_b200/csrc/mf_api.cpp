@@ -1,0 +1,601 @@
+// mf_api.cpp -- the C ABI of include/mf.h: plan construction (host logic of
+// SURVEY.md §3 step 1), the stream-ordered scheduler of mf_dgemm, the
+// host-buffer entry point and the NCCL bootstrap.  Kernels live in
+// mf_mix.cu (K4/K6) and mf_leaf.cu (K5).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+
+#include "mf_internal.h"
+
+using namespace mf;
+
+struct mf_plan_st : public Plan {};
+
+namespace {
+
+thread_local std::string g_err;
+
+mf_status fail(mf_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+mf_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(MF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define MF_CUDA(call, what)                           \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+Nccl* nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // Prefer the NCCL already loaded into the process (torch's), else the loader path.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.h = h;
+    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+    n.Reduce = (decltype(n.Reduce))dlsym(h, "ncclReduce");
+    n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
+    n.Broadcast = (decltype(n.Broadcast))dlsym(h, "ncclBroadcast");
+    n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
+    n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
+  });
+  return n.h && n.GetUniqueId && n.CommInitRank && n.Reduce && n.AllReduce && n.Broadcast ? &n
+                                                                                        : nullptr;
+}
+
+mf_status nccl_fail(Nccl* n, ncclResult_t r, const char* what) {
+  return fail(MF_ERR_NCCL, "%s: %s", what, n && n->GetErrorString ? n->GetErrorString(r) : "?");
+}
+
+// ---------------------------------------------------------------- triple algebra
+// Exact Brent check of <U,V,W> (p^2 x R each).  Dyadic
+// coefficients are scaled to integers by 2^d per matrix; the identity becomes
+// sum_q U'V'W' = 2^(dU+dV+dW) * [k==k' && i==i' && j==j'], checked in __int128.
+mf_status brent_check(int p, int R, const double* U, const double* V, const double* W) {
+  const int P2 = p * p;
+  int dexp[3] = {0, 0, 0};
+  const double* mats[3] = {U, V, W};
+  for (int t = 0; t < 3; ++t)
+    for (int i = 0; i < P2 * R; ++i) {
+      double x = mats[t][i];
+      if (!std::isfinite(x)) return fail(MF_ERR_BAD_TRIPLE, "non-finite coefficient");
+      int d = 0;
+      while (x != std::floor(x) && d < 30) { x *= 2.0; ++d; }
+      if (x != std::floor(x) || std::fabs(x) > 1e6)
+        return fail(MF_ERR_UNSUPPORTED,
+                    "coefficient %g is not an integer or a dyadic rational of modest size",
+                    mats[t][i]);
+      dexp[t] = std::max(dexp[t], d);
+    }
+  std::vector<int64_t> Ui(P2 * R), Vi(P2 * R), Wi(P2 * R);
+  for (int i = 0; i < P2 * R; ++i) {
+    Ui[i] = (int64_t)std::ldexp(U[i], dexp[0]);
+    Vi[i] = (int64_t)std::ldexp(V[i], dexp[1]);
+    Wi[i] = (int64_t)std::ldexp(W[i], dexp[2]);
+  }
+  const __int128 one = (__int128)1 << (dexp[0] + dexp[1] + dexp[2]);
+  int64_t bad = 0;
+  int fx = -1, fy = -1, fz = -1;
+  for (int x = 0; x < P2; ++x)
+    for (int y = 0; y < P2; ++y)
+      for (int z = 0; z < P2; ++z) {
+        __int128 s = 0;
+        for (int q = 0; q < R; ++q)
+          s += (__int128)Ui[x * R + q] * Vi[y * R + q] * Wi[z * R + q];
+        const int i = x / p, k = x % p, k2 = y / p, j = y % p, i2 = z / p, j2 = z % p;
+        const __int128 expect = (k == k2 && i == i2 && j == j2) ? one : 0;
+        if (s != expect) {
+          if (bad == 0) { fx = x; fy = y; fz = z; }
+          ++bad;
+        }
+      }
+  if (bad)
+    return fail(MF_ERR_BAD_TRIPLE,
+                "Brent equations violated: %lld of %lld fail; first (x,y,z) = (%d,%d,%d)",
+                (long long)bad, (long long)P2 * P2 * P2, fx, fy, fz);
+  for (int q = 0; q < R; ++q) {
+    bool u = false, v = false;
+    for (int k = 0; k < P2; ++k) { u |= U[k * R + q] != 0.0; v |= V[k * R + q] != 0.0; }
+    if (!u || !v) return fail(MF_ERR_BAD_TRIPLE, "product column %d has an all-zero operand", q);
+  }
+  return MF_OK;
+}
+
+// Kronecker composition outer (x) inner with the
+// row interleave of SPEC.md L244: outer block b, inner block s ->
+// row ((b/po)*pi + s/pi) * (po*pi) + (b%po)*pi + s%pi; product q = qo*Ri + qi.
+void kron(int po, int64_t Ro, const std::vector<double>& Uo, const std::vector<double>& Vo,
+          const std::vector<double>& Wo, int pi, int64_t Ri, const double* Ui, const double* Vi,
+          const double* Wi, std::vector<double>& U, std::vector<double>& V, std::vector<double>& W) {
+  const int P = po * pi;
+  const int64_t R = Ro * Ri;
+  U.assign((size_t)P * P * R, 0.0);
+  V.assign(U.size(), 0.0);
+  W.assign(U.size(), 0.0);
+  for (int b = 0; b < po * po; ++b)
+    for (int s = 0; s < pi * pi; ++s) {
+      const int row = ((b / po) * pi + s / pi) * P + (b % po) * pi + s % pi;
+      for (int64_t qo = 0; qo < Ro; ++qo)
+        for (int64_t qi = 0; qi < Ri; ++qi) {
+          const int64_t q = qo * Ri + qi;
+          U[row * R + q] = Uo[b * Ro + qo] * Ui[s * Ri + qi];
+          V[row * R + q] = Vo[b * Ro + qo] * Vi[s * Ri + qi];
+          W[row * R + q] = Wo[b * Ro + qo] * Wi[s * Ri + qi];
+        }
+    }
+}
+
+mf_status upload_table(MixTable& t, bool with_slots) {
+  size_t bytes = sizeof(double) * t.coef.size() + (with_slots ? sizeof(int32_t) * t.out_map.size() : 0);
+  if (bytes == 0) return MF_OK;
+  MF_CUDA(cudaMalloc(&t.d_coef, bytes), "cudaMalloc(coefficient table)");
+  std::vector<uint8_t> host(bytes);
+  memcpy(host.data(), t.coef.data(), sizeof(double) * t.coef.size());
+  if (with_slots)
+    memcpy(host.data() + sizeof(double) * t.coef.size(), t.out_map.data(),
+           sizeof(int32_t) * t.out_map.size());
+  MF_CUDA(cudaMemcpy(t.d_coef, host.data(), bytes, cudaMemcpyHostToDevice), "upload table");
+  return MF_OK;
+}
+
+void free_plan(Plan* pl) {
+  if (!pl) return;
+  DeviceGuard g(pl->device);
+  cudaDeviceSynchronize();
+  for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_coef,
+                  (void*)pl->mixB.d_coef, (void*)pl->mixC.d_coef, (void*)pl->hA, (void*)pl->hB,
+                  (void*)pl->hC})
+    if (p) cudaFree(p);
+  if (pl->done) cudaEventDestroy(pl->done);
+}
+
+bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t n) {
+  auto lo1 = reinterpret_cast<uintptr_t>(X), hi1 = lo1 + 8 * ((n - 1) * ldx + n);
+  auto lo2 = reinterpret_cast<uintptr_t>(Y), hi2 = lo2 + 8 * ((n - 1) * ldy + n);
+  return lo1 < hi2 && lo2 < hi1;
+}
+
+mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   const double* T, const double* S, double* out, int64_t ldo, int64_t stride,
+                   double alpha, cudaStream_t s) {
+  LeafArgs a;
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
+  a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
+  a.P = pl.P; a.m = pl.m;
+  a.out = out; a.ldo = ldo; a.out_block_stride = stride; a.alpha = alpha;
+  a.jobs = pl.d_jobs; a.n_jobs = pl.n_jobs;
+  MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
+  return MF_OK;
+}
+
+}  // namespace
+
+// =========================================================================== ABI
+extern "C" {
+
+const char* mf_last_error(void) { return g_err.c_str(); }
+
+const char* mf_version(void) { return "mf 0.1.0 sm_100a"; }
+
+mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const double* V,
+                  const double* W, int32_t levels, int64_t n, const mf_options* opt) {
+  g_err.clear();
+  if (!out) return fail(MF_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(MF_ERR_INVALID_ARG, "n must be >= 1 (got %lld)", (long long)n);
+  if (levels < 0) return fail(MF_ERR_INVALID_ARG, "levels must be >= 0 (got %d)", levels);
+  if (levels > 0 && (p < 1 || R < 1 || !U || !V || !W))
+    return fail(MF_ERR_INVALID_ARG, "levels > 0 needs p >= 1, R >= 1 and U, V, W");
+  mf_options o{};
+  o.device = -1;
+  if (opt) {
+    if (opt->struct_size != 0 && opt->struct_size != (int32_t)sizeof(mf_options))
+      return fail(MF_ERR_INVALID_ARG, "mf_options.struct_size %d != %d", opt->struct_size,
+                  (int)sizeof(mf_options));
+    o = *opt;
+  }
+  if (o.leaf != MF_LEAF_DMMA && o.leaf != MF_LEAF_SIMPLE)
+    return fail(MF_ERR_INVALID_ARG, "unknown leaf kind %d", o.leaf);
+  const int shard_count = o.shard_count > 1 ? o.shard_count : 1;
+  if (o.shard_rank < 0 || o.shard_rank >= shard_count)
+    return fail(MF_ERR_INVALID_ARG, "shard_rank %d outside [0, %d)", o.shard_rank, shard_count);
+
+  if (levels > 0) {
+    mf_status st = brent_check(p, R, U, V, W);
+    if (st != MF_OK) return st;
+  }
+  int64_t P = 1, RL = 1;
+  for (int l = 0; l < levels; ++l) {
+    if (n % (P * p) != 0)
+      return fail(MF_ERR_INDIVISIBLE,
+                  "n = %lld is not divisible by p^%d = %lld (p = %d, levels = %d)", (long long)n,
+                  l + 1, (long long)(P * p), p, levels);
+    P *= p;
+    RL *= R;
+  }
+  if (P > 9) return fail(MF_ERR_UNSUPPORTED, "flattened split factor p^levels = %lld > 9", (long long)P);
+  if (P * P * RL > 28000)
+    return fail(MF_ERR_UNSUPPORTED, "flattened triple too large for the post-add table (%lld x %lld)",
+                (long long)(P * P), (long long)RL);
+  if (shard_count > RL)
+    return fail(MF_ERR_INVALID_ARG, "shard_count %d exceeds the %lld leaf products", shard_count,
+                (long long)RL);
+
+  DeviceGuard guard(o.device);
+  if (!guard.ok) return fail(MF_ERR_CUDA, "cannot select device %d", o.device);
+  std::unique_ptr<mf_plan_st> pl(new (std::nothrow) mf_plan_st());
+  if (!pl) return fail(MF_ERR_OUT_OF_MEMORY, "host allocation");
+  MF_CUDA(cudaGetDevice(&pl->device), "cudaGetDevice");
+  pl->p = p; pl->R = R; pl->levels = levels; pl->n = n;
+  pl->P = (int)P; pl->RL = RL; pl->m = n / P;
+  pl->opt = o; pl->leaf = o.leaf;
+  pl->shard_rank = o.shard_rank; pl->shard_count = shard_count;
+  pl->nccl_comm = o.nccl_comm;
+
+  // ---- flatten: U^(x)L etc. (a5 of SURVEY.md §8a executed as one level) ----
+  if (levels == 0) {
+    pl->U = {1.0}; pl->V = {1.0}; pl->W = {1.0};
+  } else {
+    std::vector<double> u(U, U + p * p * R), v(V, V + p * p * R), w(W, W + p * p * R);
+    int64_t pc = p, rc = R;
+    for (int l = 1; l < levels; ++l) {
+      std::vector<double> u2, v2, w2;
+      kron((int)pc, rc, u, v, w, p, R, U, V, W, u2, v2, w2);
+      u.swap(u2); v.swap(v2); w.swap(w2);
+      pc *= p; rc *= R;
+    }
+    pl->U.swap(u); pl->V.swap(v); pl->W.swap(w);
+  }
+
+  // ---- classify operand columns: single +-1 entry => alias ----
+  const int NB = pl->P * pl->P;
+  pl->prods.resize(RL);
+  for (int64_t q = 0; q < RL; ++q) {
+    Product& pr = pl->prods[q];
+    pr.sign = 1;
+    pr.shard = (int32_t)((q * shard_count) / RL);
+    for (int side = 0; side < 2; ++side) {
+      const std::vector<double>& M = side == 0 ? pl->U : pl->V;
+      int nnz = 0, k0 = -1;
+      for (int k = 0; k < NB; ++k)
+        if (M[k * RL + q] != 0.0) { ++nnz; if (k0 < 0) k0 = k; }
+      const bool alias = nnz == 1 && std::fabs(M[k0 * RL + q]) == 1.0;
+      int32_t& src = side == 0 ? pr.a_src : pr.b_src;
+      int32_t& idx = side == 0 ? pr.a_idx : pr.b_idx;
+      if (alias) {
+        src = SRC_INPUT;
+        idx = k0;
+        if (M[k0 * RL + q] < 0) pr.sign = -pr.sign;
+      } else {
+        src = SRC_WORKSPACE;
+        std::vector<int32_t>& cols = side == 0 ? pl->mat_a_col : pl->mat_b_col;
+        idx = (int32_t)cols.size();
+        cols.push_back((int32_t)q);
+      }
+    }
+  }
+  pl->n_mat_a = (int)pl->mat_a_col.size();
+  pl->n_mat_b = (int)pl->mat_b_col.size();
+  for (int64_t q = 0; q < RL; ++q)
+    if (pl->prods[q].shard == pl->shard_rank) pl->my_prods.push_back((int32_t)q);
+
+  // ---- mix tables for this shard ----
+  for (int side = 0; side < 2 && levels > 0; ++side) {
+    MixTable& t = side == 0 ? pl->mixA : pl->mixB;
+    const std::vector<double>& M = side == 0 ? pl->U : pl->V;
+    t.nin = NB;
+    for (int32_t q : pl->my_prods) {
+      const Product& pr = pl->prods[q];
+      if ((side == 0 ? pr.a_src : pr.b_src) != SRC_WORKSPACE) continue;
+      for (int k = 0; k < NB; ++k) t.coef.push_back(M[k * RL + q]);
+      t.out_map.push_back(side == 0 ? pr.a_idx : pr.b_idx);
+      ++t.nout;
+    }
+  }
+  if (levels > 0) {
+    MixTable& c = pl->mixC;
+    c.nin = (int)RL;
+    c.nout = NB;
+    c.coef.assign((size_t)NB * RL, 0.0);
+    for (int32_t q : pl->my_prods)
+      for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+  }
+
+  // ---- device allocations ----
+  const int64_t mm = pl->m * pl->m;
+  if (levels > 0) {
+    size_t tb = sizeof(double) * mm * pl->n_mat_a, sb = sizeof(double) * mm * pl->n_mat_b,
+           pb = sizeof(double) * mm * RL;
+    if (tb && cudaMalloc(&pl->T, tb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace T (%zu bytes)", tb); }
+    if (sb && cudaMalloc(&pl->S, sb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace S (%zu bytes)", sb); }
+    if (cudaMalloc(&pl->Pw, pb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace P (%zu bytes)", pb); }
+    pl->ws_bytes = tb + sb + pb;
+    mf_status st;
+    if ((st = upload_table(pl->mixA, true)) != MF_OK ||
+        (st = upload_table(pl->mixB, true)) != MF_OK ||
+        (st = upload_table(pl->mixC, false)) != MF_OK) {
+      free_plan(pl.get());
+      return st;
+    }
+  }
+  std::vector<LeafJob> jobs;
+  for (int32_t q : pl->my_prods) {
+    const Product& pr = pl->prods[q];
+    LeafJob j;
+    j.a_coord = pr.a_src == SRC_INPUT ? ((pr.a_idx / pl->P) << 16) | (pr.a_idx % pl->P) : pr.a_idx;
+    j.b_coord = pr.b_src == SRC_INPUT ? ((pr.b_idx / pl->P) << 16) | (pr.b_idx % pl->P) : pr.b_idx;
+    j.flags = (pr.a_src == SRC_WORKSPACE ? 1 : 0) | (pr.b_src == SRC_WORKSPACE ? 2 : 0);
+    j.out_idx = levels > 0 ? q : 0;
+    jobs.push_back(j);
+  }
+  pl->n_jobs = (int)jobs.size();
+  if (!jobs.empty()) {
+    if (cudaMalloc(&pl->d_jobs, sizeof(LeafJob) * jobs.size()) != cudaSuccess) {
+      free_plan(pl.get());
+      return fail(MF_ERR_OUT_OF_MEMORY, "job table");
+    }
+    cudaMemcpy(pl->d_jobs, jobs.data(), sizeof(LeafJob) * jobs.size(), cudaMemcpyHostToDevice);
+  }
+  if (cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming) != cudaSuccess) {
+    free_plan(pl.get());
+    return fail(MF_ERR_CUDA, "cudaEventCreate");
+  }
+  *out = pl.release();
+  return MF_OK;
+}
+
+mf_status mf_destroy(mf_plan_t plan) {
+  g_err.clear();
+  if (!plan) return MF_OK;
+  free_plan(plan);
+  delete plan;
+  return MF_OK;
+}
+
+mf_status mf_plan_info(mf_plan_t pl, size_t* ws, int64_t* leaf_n, int64_t* n_products,
+                       int32_t* n_mat_a, int32_t* n_mat_b) {
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (ws) *ws = pl->ws_bytes;
+  if (leaf_n) *leaf_n = pl->m;
+  if (n_products) *n_products = pl->RL;
+  if (n_mat_a) *n_mat_a = pl->n_mat_a;
+  if (n_mat_b) *n_mat_b = pl->n_mat_b;
+  return MF_OK;
+}
+
+mf_status mf_plan_products(mf_plan_t pl, int32_t* a_src, int32_t* a_idx, int32_t* b_src,
+                           int32_t* b_idx, int32_t* sign, int32_t* shard) {
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  for (int64_t q = 0; q < pl->RL; ++q) {
+    const Product& pr = pl->prods[q];
+    if (a_src) a_src[q] = pr.a_src;
+    if (a_idx) a_idx[q] = pr.a_idx;
+    if (b_src) b_src[q] = pr.b_src;
+    if (b_idx) b_idx[q] = pr.b_idx;
+    if (sign) sign[q] = pr.sign;
+    if (shard) shard[q] = pr.shard;
+  }
+  return MF_OK;
+}
+
+static mf_status check_mat(const char* name, const void* X, int64_t ld, int64_t n) {
+  if (!X) return fail(MF_ERR_INVALID_ARG, "%s is NULL", name);
+  if (ld < n) return fail(MF_ERR_INVALID_ARG, "ld%s = %lld < n = %lld", name, (long long)ld, (long long)n);
+  if (reinterpret_cast<uintptr_t>(X) % 8) return fail(MF_ERR_INVALID_ARG, "%s is not 8-byte aligned", name);
+  return MF_OK;
+}
+
+mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
+                   int64_t ldb, double* C, int64_t ldc, void* stream) {
+  g_err.clear();
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  const int64_t n = pl->n;
+  const bool root_inputs = pl->nccl_comm && pl->opt.input_mode == MF_IN_ROOT;
+  const bool is_root = pl->shard_rank == 0;
+  mf_status st;
+  if (!root_inputs || is_root) {
+    if ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK)
+      return st;
+  }
+  if ((st = check_mat("C", C, ldc, n)) != MF_OK) return st;
+  if ((A && overlaps(A, lda, C, ldc, n)) || (B && overlaps(B, ldb, C, ldc, n)))
+    return fail(MF_ERR_INVALID_ARG, "C overlaps A or B");
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  Nccl* nc = nullptr;
+  if (pl->nccl_comm) {
+    nc = nccl();
+    if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  }
+  if (root_inputs) {
+    // Broadcast rank 0's A and B into plan-owned replicas (contiguous, ld n).
+    const size_t bytes = sizeof(double) * n * n;
+    if (!pl->hA && cudaMalloc(&pl->hA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica A");
+    if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica B");
+    if (is_root) {
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy A");
+      MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy B");
+    }
+    ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
+    ncclResult_t r;
+    if ((r = nc->Broadcast(pl->hA, pl->hA, (size_t)n * n, ncclDouble, 0, comm, s)) != ncclSuccess)
+      return nccl_fail(nc, r, "ncclBroadcast(A)");
+    if ((r = nc->Broadcast(pl->hB, pl->hB, (size_t)n * n, ncclDouble, 0, comm, s)) != ncclSuccess)
+      return nccl_fail(nc, r, "ncclBroadcast(B)");
+    A = pl->hA; lda = n; B = pl->hB; ldb = n;
+  }
+
+  if (pl->levels == 0) {
+    if ((st = run_leaf(*pl, A, lda, B, ldb, nullptr, nullptr, C, ldc, 0, alpha, s)) != MF_OK) return st;
+  } else {
+    // a1, a2: fused pre-additions (K4) for this shard's materialised operands
+    MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
+    MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
+    // a3: all leaf products in one launch (K5)
+    if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) != MF_OK)
+      return st;
+    // a4: fused post-addition (K6)
+    MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
+  }
+  if (pl->nccl_comm) {
+    // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
+    ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
+    if (ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");
+    ncclResult_t r = pl->opt.output_mode == MF_OUT_ALL
+                         ? nc->AllReduce(C, C, (size_t)n * n, ncclDouble, ncclSum, comm, s)
+                         : nc->Reduce(C, C, (size_t)n * n, ncclDouble, ncclSum, 0, comm, s);
+    if (r != ncclSuccess) return nccl_fail(nc, r, "ncclReduce(C)");
+  }
+  return MF_OK;
+}
+
+mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* C, int64_t ldc, void* stream) {
+  g_err.clear();
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  const int64_t n = pl->n;
+  mf_status st;
+  if ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK ||
+      (st = check_mat("C", C, ldc, n)) != MF_OK)
+    return st;
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(double) * n * n;
+  if (!pl->hA && cudaMalloc(&pl->hA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device A");
+  if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B");
+  if (!pl->hC && cudaMalloc(&pl->hC, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C");
+  MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+  MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
+  mf_options saved = pl->opt;
+  pl->opt.input_mode = MF_IN_REPLICATED;
+  st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
+  pl->opt = saved;
+  if (st != MF_OK) return st;
+  MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+  MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  return MF_OK;
+}
+
+mf_status mf_premix(mf_plan_t pl, int32_t side, const double* X, int64_t ldx, double* out,
+                    void* stream) {
+  g_err.clear();
+  if (!pl || !X || !out || (side != 0 && side != 1)) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no pre-additions");
+  DeviceGuard guard(pl->device);
+  MF_CUDA(launch_premix(*pl, side == 0 ? pl->mixA : pl->mixB, X, ldx, out,
+                        static_cast<cudaStream_t>(stream)),
+          "pre-add (K4)");
+  return MF_OK;
+}
+
+mf_status mf_leaf(mf_plan_t pl, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  const double* T, const double* S, double* P, void* stream) {
+  g_err.clear();
+  if (!pl || !A || !B || !P) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  DeviceGuard guard(pl->device);
+  return run_leaf(*pl, A, lda, B, ldb, T, S, P, pl->m, pl->m * pl->m, 1.0,
+                  static_cast<cudaStream_t>(stream));
+}
+
+mf_status mf_postmix(mf_plan_t pl, double alpha, const double* P, double* C, int64_t ldc,
+                     void* stream) {
+  g_err.clear();
+  if (!pl || !P || !C) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no post-addition");
+  DeviceGuard guard(pl->device);
+  MF_CUDA(launch_postmix(*pl, alpha, P, C, ldc, static_cast<cudaStream_t>(stream)), "post-add (K6)");
+  return MF_OK;
+}
+
+mf_status mf_nccl_unique_id(void* id_out) {
+  g_err.clear();
+  Nccl* nc = nccl();
+  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  if (!id_out) return fail(MF_ERR_INVALID_ARG, "id_out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = nc->GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclGetUniqueId");
+  memcpy(id_out, &id, sizeof id);
+  return MF_OK;
+}
+
+mf_status mf_nccl_comm_create(void** comm_out, const void* id, int32_t rank, int32_t nranks) {
+  g_err.clear();
+  Nccl* nc = nccl();
+  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  if (!comm_out || !id || rank < 0 || rank >= nranks) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  ncclComm_t comm;
+  ncclResult_t r = nc->CommInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclCommInitRank");
+  *comm_out = comm;
+  return MF_OK;
+}
+
+mf_status mf_nccl_comm_destroy(void* comm) {
+  g_err.clear();
+  if (!comm) return MF_OK;
+  Nccl* nc = nccl();
+  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  ncclResult_t r = nc->CommDestroy(static_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclCommDestroy");
+  return MF_OK;
+}
+
+}  // extern "C"

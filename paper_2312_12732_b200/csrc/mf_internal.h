@@ -1,0 +1,103 @@
+// mf_internal.h -- plan structure and kernel launchers shared by the libmf.so
+// translation units (product path only; nothing here is shared with oracle/).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mf.h"
+
+namespace mf {
+
+// Largest flattened split factor P = p^levels the mix kernels are built for
+// (P^2 <= 81 blocks: p=9 one level, p=3 two levels, p=2 up to three levels).
+constexpr int kMaxBlocks = 81;
+
+// Operand source of a leaf product (mf_plan_products: a_src / b_src).
+enum Src : int32_t { SRC_INPUT = 0, SRC_WORKSPACE = 1 };
+
+// One leaf product P_q' = X_q * Y_q of the flattened triple.
+struct Product {
+  int32_t a_src, a_idx;  // A-block index (SRC_INPUT) or T slot (SRC_WORKSPACE)
+  int32_t b_src, b_idx;  // B-block index or S slot
+  int32_t sign;          // +-1 folded out of aliased operands
+  int32_t shard;         // shard that computes it
+};
+
+// Device-side routing entry of the leaf kernel (kept POD, 16 bytes).
+struct LeafJob {
+  int32_t a_coord;  // SRC_INPUT: (block_row << 16) | block_col; SRC_WORKSPACE: slot
+  int32_t b_coord;
+  int32_t flags;    // bit0: A from workspace, bit1: B from workspace
+  int32_t out_idx;  // index of the output block in P (or 0 with direct C output)
+};
+
+// Coefficient table of one mix kernel launch: nout outputs, each a
+// combination of up to nin inputs, coef[o * nin + k] (0 = absent).
+struct MixTable {
+  int nin = 0, nout = 0;
+  std::vector<double> coef;      // nout x nin
+  std::vector<int32_t> out_map;  // output o -> slot / C block it writes
+  double* d_coef = nullptr;      // device copy (owned by the plan)
+};
+
+struct Plan {
+  int device = 0;
+  int p = 1, R = 1, levels = 0;
+  int64_t n = 0;
+  // flattened triple: P = p^levels, RL = R^levels; U/V/W are P^2 x RL row-major
+  int P = 1;
+  int64_t RL = 1, m = 0;
+  std::vector<double> U, V, W;
+  std::vector<Product> prods;
+  int n_mat_a = 0, n_mat_b = 0;         // materialised T / S slots (whole triple)
+  std::vector<int32_t> mat_a_col, mat_b_col;  // slot -> product column q
+  mf_options opt{};
+  int leaf = MF_LEAF_DMMA;
+  int shard_rank = 0, shard_count = 1;
+  // shard-local view: the products this plan's rank computes
+  std::vector<int32_t> my_prods;  // product indices q
+  MixTable mixA, mixB;            // pre-additions for the slots my_prods use
+  MixTable mixC;                  // post-addition over ALL products (zero coef outside shard)
+  // device memory
+  double* T = nullptr;   // n_mat_a x m x m
+  double* S = nullptr;   // n_mat_b x m x m
+  double* Pw = nullptr;  // RL x m x m (leaf outputs)
+  size_t ws_bytes = 0;
+  LeafJob* d_jobs = nullptr;  // my_prods.size() jobs
+  int n_jobs = 0;
+  // host-buffer path (mf_dgemm_host): device copies of A, B, C
+  double *hA = nullptr, *hB = nullptr, *hC = nullptr;
+  // NCCL
+  void* nccl_comm = nullptr;
+  cudaEvent_t done = nullptr;
+};
+
+// ---- launchers (mf_mix.cu, mf_leaf.cu); return cudaError_t of the launch ----
+cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
+                          double* out, cudaStream_t s);
+cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C,
+                           int64_t ldc, cudaStream_t s);
+
+struct LeafArgs {
+  // operand views: matrices (4-D block view, SRC_INPUT) and workspaces (3-D)
+  const double* A; int64_t lda;
+  const double* B; int64_t ldb;
+  const double* T; const double* S;
+  int n_slots_a, n_slots_b;
+  int P;          // blocks per side of the input partition
+  int64_t m;      // leaf side
+  double* out;    // output base: P workspace (ld m, block stride m*m) or C
+  int64_t ldo;
+  int64_t out_block_stride;  // elements between consecutive output blocks (0 => single)
+  double alpha;
+  const LeafJob* jobs; int n_jobs;
+};
+bool leaf_tma_supported(const LeafArgs& a);
+cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s);
+
+}  // namespace mf

@@ -1,0 +1,388 @@
+// mf_leaf.cu -- K5: the batched leaf products P_q' = X_q * Y_q of Eq.
+// "strassen" ("There are seven products, each product can
+// be done recursively"), here all R^L products of the flattened triple in ONE
+// launch, fp64 on the B200 FP64 tensor path.
+//
+// B200 design:
+//  * FP64 tensor math on sm_100a is the legacy warp-level mma.sync.m8n8k4.f64
+//    (SASS DMMA.8x8x4); tcgen05 has no f64 kind.  Measured: 37.1 TF/s with
+//    register-resident operands (tools/peaks_fp64.cu) = 64 FMA/clk/SM.
+//  * Operands are staged into shared memory by TMA (cp.async.bulk.tensor)
+//    with an mbarrier ring of STAGES slots.  8 MMA warps (2 per SM
+//    sub-partition, so each may hold 255 registers); lane 0 of warp 0 issues
+//    the TMA for slot kb+STAGES-1 once all warps released it (empty barrier).
+//  * Operand views: an aliased operand is block (br, bc) of the caller's A/B,
+//    addressed through a 4-D tensor map {col, block-col, row, block-row} so
+//    TMA zero-fills past the block edge (ragged leaves never read a
+//    neighbouring block); a materialised operand is a slot of the T/S
+//    workspace (3-D map {col, row, slot}).
+//  * CTA tile 128x128x16.  Each MMA warp owns 64x32 of C: 64 fp64
+//    accumulators per thread.  Fragments are fetched with 128-bit LDS:
+//      A (SWIZZLE_128B, rows of 16 k): lane (r=L/4, kk=L%4) loads
+//        A[r][2kk], A[r][2kk+1] -> the k-permutation k = 8g + 2kk + s feeds
+//        two k-steps s = 0,1 (conflict-free: 4 wavefronts per 512 B);
+//      B (no swizzle, rows of 128 n): lane (kk=L%4, nn=L/4) loads
+//        B[8g+2kk+s][2nn], B[..][2nn+1] -> the n-permutation n = 2c + j feeds
+//        two n-subtiles j = 0,1; each thread then owns 4 CONSECUTIVE output
+//        columns, stored with one 256-bit st.global.v4.f64.
+//  * Grid = products x tiles, 1 CTA/SM (256 threads, ~164 KB smem); tiles of
+//    a product are rasterised in groups of 8 tile-rows for L2 reuse.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "mf_internal.h"
+
+namespace mf {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int STAGES = 5;
+constexpr int MMA_WARPS = 8;
+constexpr int THREADS = MMA_WARPS * 32;
+constexpr int A_BYTES = BM * BK * 8;
+constexpr int B_BYTES = BK * BN * 8;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+constexpr int GROUP_M = 8;
+
+struct LeafParams {
+  int64_t m;
+  int tiles_m, tiles_n, kblocks;
+  double* out;
+  int64_t ldo, out_stride;
+  double alpha;
+  const LeafJob* jobs;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+         "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void lds128(uint32_t addr, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
+                 const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
+                 const LeafParams prm) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t s_base = smem_u32(smem);
+  const uint32_t full0 = s_base + STAGES * STAGE_BYTES;
+  const uint32_t empty0 = full0 + STAGES * 8;
+
+  // ---- tile -> (product job, tm, tn), grouped rasterisation ----
+  const int tiles_per_job = prm.tiles_m * prm.tiles_n;
+  const int job_id = blockIdx.x / tiles_per_job;
+  const int t = blockIdx.x - job_id * tiles_per_job;
+  const int group_tiles = GROUP_M * prm.tiles_n;
+  const int first_m = (t / group_tiles) * GROUP_M;
+  const int gsz = min(prm.tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (t % group_tiles) % gsz;
+  const int tn = (t % group_tiles) / gsz;
+  const LeafJob job = prm.jobs[job_id];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, MMA_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---- TMA producer: warp 0 refills the slot freed one iteration earlier ----
+  const bool a_ws = job.flags & 1, b_ws = job.flags & 2;
+  const CUtensorMap* mapA = a_ws ? &tmT : &tmA;
+  const CUtensorMap* mapB = b_ws ? &tmS : &tmB;
+  const int a_br = job.a_coord >> 16, a_bc = job.a_coord & 0xffff;
+  const int b_br = job.b_coord >> 16, b_bc = job.b_coord & 0xffff;
+  auto issue = [&](int kb) {
+    const int s = kb % STAGES;
+    const uint32_t fb = full0 + 8 * s;
+    mbar_expect_tx(fb, STAGE_BYTES);
+    const uint32_t dA = s_base + s * STAGE_BYTES, dB = dA + A_BYTES;
+    if (a_ws) tma_load_3d(dA, mapA, fb, kb * BK, tm * BM, job.a_coord);
+    else      tma_load_4d(dA, mapA, fb, kb * BK, a_bc, tm * BM, a_br);
+    if (b_ws) tma_load_3d(dB, mapB, fb, tn * BN, kb * BK, job.b_coord);
+    else      tma_load_4d(dB, mapB, fb, tn * BN, b_bc, kb * BK, b_br);
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapB)) : "memory");
+    for (int kb = 0; kb < STAGES - 1 && kb < prm.kblocks; ++kb) issue(kb);
+  }
+
+  // ================= MMA warps =================
+  const int wm = warp >> 2;  // 0..1 -> 64-row half
+  const int wn = warp & 3;   // 0..3 -> 32-col quarter
+  const int lr = lane >> 2, lk = lane & 3;
+
+  double acc[8][2][2][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) { acc[i][j][u][0] = 0.0; acc[i][j][u][1] = 0.0; }
+
+  // per-lane shared-memory offsets (bytes) inside a stage
+  uint32_t offA[2];
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+    offA[g] = (wm * 64 + lr) * 128 + ((((4 * g + lk) ^ lr) & 7) << 4);
+  const uint32_t offB = (2 * lk) * (BN * 8) + (wn * 32 + 2 * lr) * 8;
+
+  for (int kb = 0; kb < prm.kblocks; ++kb) {
+    if (warp == 0) {
+      const int kn = kb + STAGES - 1;  // refill the slot consumed at kb - 1
+      if (kn < prm.kblocks) {
+        if (kb > 0) mbar_wait(empty0 + 8 * (kn % STAGES), ((kb - 1) / STAGES) & 1);
+        if (lane == 0) issue(kn);
+      }
+    }
+    const int s = kb % STAGES;
+    mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+    const uint32_t sA = s_base + s * STAGE_BYTES, sB = sA + A_BYTES;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      double a[8][2];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, a[mi][0], a[mi][1]);
+      double b[2][2][2];  // [nj][s][j]
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+          lds128(sB + offB + (8 * g + s2) * (BN * 8) + nj * 16 * 8, b[nj][s2][0], b[nj][s2][1]);
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              dmma(acc[mi][nj][j][0], acc[mi][nj][j][1], a[mi][s2], b[nj][s2][j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * s);
+  }
+
+  // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
+  double* out = prm.out + (int64_t)job.out_idx * prm.out_stride;
+  const double alpha = prm.alpha;
+  const bool vec_ok = ((prm.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 31) == 0);
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
+    if (row >= prm.m) continue;
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      const int64_t col = (int64_t)tn * BN + wn * 32 + nj * 16 + 4 * lk;
+      double v0 = acc[mi][nj][0][0], v1 = acc[mi][nj][1][0];
+      double v2 = acc[mi][nj][0][1], v3 = acc[mi][nj][1][1];
+      if (alpha != 1.0) {
+        v0 = __dmul_rn(alpha, v0); v1 = __dmul_rn(alpha, v1);
+        v2 = __dmul_rn(alpha, v2); v3 = __dmul_rn(alpha, v3);
+      }
+      double* dst = out + row * prm.ldo + col;
+      if (vec_ok && col + 3 < prm.m) {
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                     :: "l"(dst), "d"(v0), "d"(v1), "d"(v2), "d"(v3) : "memory");
+      } else {
+        if (col + 0 < prm.m) dst[0] = v0;
+        if (col + 1 < prm.m) dst[1] = v1;
+        if (col + 2 < prm.m) dst[2] = v2;
+        if (col + 3 < prm.m) dst[3] = v3;
+      }
+    }
+  }
+}
+
+// MF_LEAF_SIMPLE: one thread per output element, k ascending, fma.rn.f64.
+// Any shape/alignment; an ablation and the fallback for views TMA cannot
+// describe (odd m or odd leading dimension).
+struct SimpleParams {
+  const double *A, *B, *T, *S;
+  int64_t lda, ldb, m;
+  double* out;
+  int64_t ldo, out_stride;
+  double alpha;
+  const LeafJob* jobs;
+};
+
+__global__ void leaf_simple_kernel(const SimpleParams prm) {
+  const LeafJob job = prm.jobs[blockIdx.z];
+  const int64_t r = (int64_t)blockIdx.y * 16 + threadIdx.y;
+  const int64_t c = (int64_t)blockIdx.x * 16 + threadIdx.x;
+  if (r >= prm.m || c >= prm.m) return;
+  const int64_t mm = prm.m * prm.m;
+  const double* X;
+  int64_t ldx;
+  if (job.flags & 1) { X = prm.T + job.a_coord * mm; ldx = prm.m; }
+  else { X = prm.A + (job.a_coord >> 16) * prm.m * prm.lda + (job.a_coord & 0xffff) * prm.m; ldx = prm.lda; }
+  const double* Y;
+  int64_t ldy;
+  if (job.flags & 2) { Y = prm.S + job.b_coord * mm; ldy = prm.m; }
+  else { Y = prm.B + (job.b_coord >> 16) * prm.m * prm.ldb + (job.b_coord & 0xffff) * prm.m; ldy = prm.ldb; }
+  double acc = 0.0;
+  for (int64_t k = 0; k < prm.m; ++k) acc = fma(X[r * ldx + k], Y[k * ldy + c], acc);
+  if (prm.alpha != 1.0) acc = __dmul_rn(prm.alpha, acc);
+  prm.out[job.out_idx * prm.out_stride + r * prm.ldo + c] = acc;
+}
+
+// ---- tensor-map encoding through the driver entry point (no -lcuda) ----
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 4-D block view of an n x n row-major matrix: {col-in-block, block-col,
+// row-in-block, block-row}; box {bc0, 1, bc2, 1}.
+bool encode_block_view(CUtensorMap* map, const double* X, int64_t ld, int P, int64_t m,
+                       uint32_t box0, uint32_t box2, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[4] = {(cuuint64_t)m, (cuuint64_t)P, (cuuint64_t)m, (cuuint64_t)P};
+  cuuint64_t strides[3] = {(cuuint64_t)m * 8, (cuuint64_t)ld * 8, (cuuint64_t)m * ld * 8};
+  cuuint32_t box[4] = {box0, 1, box2, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D slot view of a workspace [slots][m][m]: {col, row, slot}.
+bool encode_slot_view(CUtensorMap* map, const double* X, int slots, int64_t m, uint32_t box0,
+                      uint32_t box1, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)m, (cuuint64_t)(slots > 0 ? slots : 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)m * 8, (cuuint64_t)m * m * 8};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+bool leaf_tma_supported(const LeafArgs& a) {
+  // TMA: 16-byte aligned bases, strides multiple of 16 bytes (m, ld even).
+  if (!encode_fn()) return false;
+  if ((a.m & 1) || (a.lda & 1) || (a.ldb & 1)) return false;
+  if (!al16(a.A) || !al16(a.B) || (a.T && !al16(a.T)) || (a.S && !al16(a.S))) return false;
+  if (a.m > (int64_t)1 << 30 || a.P > 0xffff) return false;
+  return true;
+}
+
+cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
+  if (a.n_jobs == 0 || a.m == 0) return cudaSuccess;
+  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a)) {
+    CUtensorMap mA, mT, mB, mS;
+    bool ok = encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+              encode_block_view(&mB, a.B, a.ldb, a.P, a.m, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+              encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM,
+                               CU_TENSOR_MAP_SWIZZLE_128B) &&
+              encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, BN, BK,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!ok) return cudaErrorInvalidValue;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(leaf_dmma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    LeafParams prm;
+    prm.m = a.m;
+    prm.tiles_m = (int)((a.m + BM - 1) / BM);
+    prm.tiles_n = (int)((a.m + BN - 1) / BN);
+    prm.kblocks = (int)((a.m + BK - 1) / BK);
+    prm.out = a.out;
+    prm.ldo = a.ldo;
+    prm.out_stride = a.out_block_stride;
+    prm.alpha = a.alpha;
+    prm.jobs = a.jobs;
+    const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
+    if (grid > 0x7fffffff) return cudaErrorInvalidValue;
+    leaf_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mT, mB, mS, prm);
+    return cudaGetLastError();
+  }
+  SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, a.out, a.ldo, a.out_block_stride,
+                   a.alpha, a.jobs};
+  dim3 grid((unsigned)((a.m + 15) / 16), (unsigned)((a.m + 15) / 16), (unsigned)a.n_jobs);
+  leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
+  return cudaGetLastError();
+}
+
+}  // namespace mf

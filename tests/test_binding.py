@@ -1,0 +1,109 @@
+"""CPU-side checks of the boundary (no GPU compute): libmf.so loads, exports
+every entry point include/mf.h declares, and mf_plan's host-side validation
+(exact Brent check, divisibility, arguments) answers with the documented
+status codes.  Also: the product catalog equals the oracle's."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2312_12732_b200 as mf
+from paper_2312_12732_b200 import triples
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "mf.h")).read()
+    return sorted(set(re.findall(r"^(?:mf_status|const char\*)\s+(mf_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    names = header_functions()
+    assert len(names) >= 14
+    lib = ctypes.CDLL(mf.LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(mf.EXPORTS)
+
+
+def test_version():
+    assert "sm_100a" in mf.version()
+
+
+@pytest.mark.parametrize("name", list(triples.CATALOG))
+def test_product_catalog_matches_oracle(name):
+    t = triples.get(name)
+    o = oracle.catalog(name)
+    assert t.p == o.p and t.R == o.R
+    assert (t.U == o.U).all() and (t.V == o.V).all() and (t.W == o.W).all()
+
+
+def _plan_status(p, R, U, V, W, levels, n, **kw):
+    h = ctypes.c_void_p()
+    opt = mf.mf_options()
+    opt.struct_size = ctypes.sizeof(mf.mf_options)
+    opt.device = -1
+    for k, v in kw.items():
+        setattr(opt, k, v)
+    args = [np.ascontiguousarray(x, dtype=np.float64) if x is not None else None for x in (U, V, W)]
+    st = mf._lib.mf_plan(ctypes.byref(h), p, R, *[a.ctypes.data if a is not None else None
+                                                    for a in args], levels, n, ctypes.byref(opt))
+    assert not h.value or st == 0
+    return st, mf._lib.mf_last_error().decode()
+
+
+def test_plan_rejects_bad_triple_with_first_violation():
+    t = triples.PAPER_STRASSEN
+    W = t.W.copy()
+    W[3, 0] = 0  # SPEC.md L193 mutation
+    st, msg = _plan_status(2, 7, t.U, t.V, W, 1, 64)
+    assert st == mf.MF_ERR_BAD_TRIPLE and "Brent" in msg
+    # the printed (unlabelled) c^t row order is also rejected (reading R1)
+    Wn = t.W[[0, 2, 1, 3]]
+    st, msg = _plan_status(2, 7, t.U, t.V, Wn, 1, 64)
+    assert st == mf.MF_ERR_BAD_TRIPLE and "8 of 64" in msg
+
+
+def test_plan_rejects_dead_product():
+    t = triples.STRASSEN_WINOGRAD
+    U = np.concatenate([t.U, np.zeros((4, 1))], 1)
+    V = np.concatenate([t.V, np.ones((4, 1))], 1)
+    W = np.concatenate([t.W, np.zeros((4, 1))], 1)
+    st, msg = _plan_status(2, 8, U, V, W, 1, 64)
+    assert st == mf.MF_ERR_BAD_TRIPLE and "all-zero" in msg
+
+
+def test_plan_rejects_indivisible_and_bad_args():
+    t = triples.LADERMAN
+    st, msg = _plan_status(3, 23, t.U, t.V, t.W, 1, 100)
+    assert st == mf.MF_ERR_INDIVISIBLE and "100" in msg and "p = 3" in msg
+    t = triples.STRASSEN_WINOGRAD
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 1002)  # 1002 % 4 != 0
+    assert st == mf.MF_ERR_INDIVISIBLE
+    st, _ = _plan_status(2, 7, t.U, t.V, t.W, -1, 64)
+    assert st == mf.MF_ERR_INVALID_ARG
+    st, _ = _plan_status(2, 7, t.U, t.V, t.W, 1, 0)
+    assert st == mf.MF_ERR_INVALID_ARG
+    st, _ = _plan_status(2, 7, None, None, None, 1, 64)
+    assert st == mf.MF_ERR_INVALID_ARG
+    st, _ = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, shard_rank=3, shard_count=2)
+    assert st == mf.MF_ERR_INVALID_ARG
+
+
+def test_plan_rejects_non_dyadic_coefficients():
+    t = triples.STRASSEN_WINOGRAD
+    U = t.U.copy() / 3.0
+    st, _ = _plan_status(2, 7, U, t.V, t.W, 1, 64)
+    assert st == mf.MF_ERR_UNSUPPORTED
+
+
+def test_plan_accepts_dyadic_rescaling_up_to_device():
+    """U/2, W*2 is the same bilinear map; the exact dyadic Brent check accepts it
+    (the plan then fails only for lack of a GPU here, or succeeds on one)."""
+    t = triples.STRASSEN_WINOGRAD
+    st, msg = _plan_status(2, 7, t.U / 2, t.V, t.W * 2, 1, 64)
+    assert st in (mf.MF_OK, mf.MF_ERR_CUDA, mf.MF_ERR_OUT_OF_MEMORY), msg
