@@ -1,0 +1,326 @@
+"""Bench: effective fp64 TFLOPS (2n^3/t) of the Matrix Flow hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mf|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (product-sharded, NCCL)
+
+Workload (BASELINE.json metric / config 3): n = 16384 fp64, two-level
+Strassen-Winograd executed as one level of the flattened <4,4,4;49> triple
+(49 leaf products of 4096^3).  A step = one mf_dgemm call (pre-add A, pre-add
+B, batched leaf DGEMM, post-add) on inputs already resident in HBM; inputs are
+2.1 GB each (> 126 MB L2), so no L2 flush is needed between steps.  With N > 1
+ranks the 49 products are sharded across ranks and the partial C is summed onto
+rank 0 with NCCL (strong scaling: the same problem on N GPUs).
+
+Printed (rank 0, one JSON line): value, ms_per_step, the leaf kernel's live
+roofline, classical baselines in the same run (cuBLAS DGEMM and our own
+levels=0 leaf), the max scaled error against cuBLAS, the end-to-end number
+through mf_dgemm_host (host buffers, copies inside the timed region), the
+clocks seen during the timed region and the CPU-oracle baseline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective fp64 TFLOPS (2n^3/t) at n=16384 vs classic DGEMM; max scaled error"
+UNIT = "TFLOPS"
+CPU_SAMPLE_N = 4096  # oracle sample: same triple and levels at n/4 (1/64 of the work)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["mf", "reference"], default="mf")
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--triple", default="strassen-winograd")
+    ap.add_argument("--levels", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-classical", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return f"n={a.n} fp64, {a.levels}-level {a.triple} (flattened, {_rank(a) ** a.levels} leaf products)"
+
+
+def _rank(a):
+    return {"strassen-winograd": 7, "paper-strassen": 7, "strassen-1969": 7, "laderman": 23,
+            "classical-p2": 8, "classical-p3": 27}[a.triple]
+
+
+def config(a, world):
+    return {"workload": workload_name(a), "n": a.n, "triple": a.triple, "levels": a.levels,
+            "leaf_products": _rank(a) ** a.levels, "inputs": "uniform[-1,1) fp64, seeds 0/1",
+            "l2": "inputs larger than L2 (8n^2 = %.1f GB per matrix); no flush" % (8 * a.n ** 2 / 1e9),
+            "parallelism": f"product-sharded x{world}" if world > 1 else "single GPU"}
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0])); mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def fp64_peak():
+    """Measured FP64 DMMA peak (tools/peaks_fp64.cu on this pool's B200, committed
+    under profiles/).  MEASURED_PEAKS.json carries no FP64 figure."""
+    path = os.path.join(ROOT, "profiles", "peaks_fp64.json")
+    with open(path) as f:
+        d = json.load(f)
+    return float(d["dmma_tflops"]), "measured: tools/peaks_fp64.cu DMMA m8n8k4, profiles/peaks_fp64.json"
+
+
+def leaf_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_leaf.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_baseline(a):
+    """The oracle (or_fmm: plain C interpreter of Eq. "strassen", OpenMP over
+    rows) on the host cores: same triple and levels at n = CPU_SAMPLE_N."""
+    import numpy as np
+    import mf_inputs
+    import oracle
+    n = CPU_SAMPLE_N
+    A, B = mf_inputs.pair("uniform", n, 0)
+    t = oracle.catalog(a.triple)
+    t0 = time.perf_counter()
+    oracle.fmm(A, B, t, a.levels)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} "
+                      f"(1/{(a.n // n) ** 3} of the n={a.n} work), {dt:.2f} s; value = 2n^3/t at n={n}",
+            "seconds": dt}
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle as it stands, each step one bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import mf_inputs
+    import oracle
+    n = CPU_SAMPLE_N
+    A, B = mf_inputs.pair("uniform", n, 0)
+    t = oracle.catalog(a.triple)
+    for _ in range(a.warmup):
+        oracle.fmm(A, B, t, a.levels)
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        oracle.fmm(A, B, t, a.levels)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
+    value = 2.0 * n ** 3 / dt / 1e12
+    sample = (f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} per step "
+              f"(1/{(a.n // n) ** 3} of the n={a.n} work); value = 2n^3/t at n={n}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(a, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ main arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+    import mf_inputs
+    import paper_2312_12732_b200 as mf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [mf.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = mf.nccl_comm_create(obj[0], rank, world)
+
+    n = a.n
+    triple = mf.triples.get(a.triple)
+    plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
+                   nccl_comm=comm, profile=True)
+    info = plan.info()
+    stream = torch.cuda.current_stream()
+    A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
+    C = torch.empty((n, n), dtype=torch.float64, device=dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up, then K timed steps ----
+    for _ in range(a.warmup):
+        plan.dgemm(A, B, C)
+    barrier()
+    plan.profile_read(reset=True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        plan.dgemm(A, B, C)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    phases = plan.profile_read(reset=True)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (K5 leaf), live over the timed region ----
+    my_prods = sum(1 for s in plan.products()["shard"] if s == rank)
+    m = info["leaf_n"]
+    leaf_ms = phases["leaf"] / max(1, phases["calls"])
+    leaf_flops = my_prods * 2.0 * m ** 3
+    peak, peak_src = fp64_peak()
+    achieved = leaf_flops / (leaf_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "leaf_dmma_kernel (K5)", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": leaf_traffic(),
+                "peak_source": peak_src, "flops_per_launch": leaf_flops, "ms_per_launch": leaf_ms,
+                "phase_ms_per_step": {k: phases[k] / max(1, phases["calls"]) for k in plan.PHASES},
+                "leaf_share_of_step": leaf_ms / ms}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config(a, world), "clocks": clk,
+           "gpu_launches": 4 * a.steps if a.levels > 0 else a.steps,
+           "roofline": roofline}
+
+    # ---- accuracy vs classical cuBLAS DGEMM, and the classical baselines ----
+    if rank == 0:
+        Cref = torch.empty_like(C)
+        torch.matmul(A, B, out=Cref)
+        torch.cuda.synchronize()
+        den = n * float(A.abs().max()) * float(B.abs().max())
+        out["max_scaled_error"] = float((C - Cref).abs().max()) / den
+        out["error_bound"] = 1e-13 * max(1, a.levels)
+        if not a.no_classical and world == 1:
+            def timeit(fn):
+                for _ in range(2):
+                    fn()
+                torch.cuda.synchronize()
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                for _ in range(a.steps):
+                    fn()
+                s1.record(stream)
+                torch.cuda.synchronize()
+                return s0.elapsed_time(s1) / a.steps
+            t_cublas = timeit(lambda: torch.matmul(A, B, out=Cref))
+            with mf.Plan(None, 0, n, device=local) as p0:
+                t_leaf0 = timeit(lambda: p0.dgemm(A, B, C))
+            fl = 2.0 * n ** 3 / 1e12
+            out["classical"] = {"cublas_dgemm_tflops": fl / (t_cublas * 1e-3), "cublas_ms": t_cublas,
+                                "mf_levels0_tflops": fl / (t_leaf0 * 1e-3), "mf_levels0_ms": t_leaf0}
+            out["speedup_vs_cublas"] = t_cublas / ms
+        del Cref
+
+    # ---- end to end through the C ABI with host buffers ----
+    if not a.no_e2e and world == 1:
+        Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Bh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Ch = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A); Bh.copy_(B)
+        del A, B, C
+        torch.cuda.empty_cache()
+        plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)
+        dt = (time.perf_counter() - t0) / a.steps
+        out["e2e"] = {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "ms_per_step": dt * 1e3,
+                      "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
+                      "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step)"}
+        out["gpu_launches_e2e_per_step"] = 4 if a.levels > 0 else 1
+
+    if rank == 0 and world == 1 and not a.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(a)
+
+    plan.close()
+    if comm is not None:
+        mf.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

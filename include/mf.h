@@ -67,6 +67,8 @@ typedef struct {
                            MF_IN_ROOT (rank 0's A, B are broadcast first)         */
   int32_t output_mode;  /* MF_OUT_ROOT (C summed onto rank 0) or MF_OUT_ALL
                            (C summed onto every rank)                             */
+  int32_t profile;      /* 1: mf_dgemm records CUDA events around each phase on
+                           the call's stream (read with mf_profile_read)          */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.
@@ -145,6 +147,14 @@ mf_status mf_leaf(mf_plan_t plan, const double* A, int64_t lda, const double* B,
                   const double* T, const double* S, double* P, void* stream);
 mf_status mf_postmix(mf_plan_t plan, double alpha, const double* P, double* C, int64_t ldc,
                      void* stream);
+
+/* Phase timing of a profile-enabled plan (mf_options.profile = 1): waits for
+ * the recorded events and writes the summed device time in milliseconds of
+ * each phase over the mf_dgemm calls since the last reset:
+ *   ms[0] pre-add A (K4), ms[1] pre-add B (K4), ms[2] leaf products (K5),
+ *   ms[3] post-add (K6), ms[4] NCCL exchange (0 on one GPU).
+ * *calls = number of mf_dgemm calls summed; reset != 0 clears the sums. */
+mf_status mf_profile_read(mf_plan_t plan, double* ms /* 5 */, int32_t* calls, int32_t reset);
 
 /* Multi-GPU bootstrap (NCCL over NVLink; the 128-byte unique id is exchanged
  * by the caller, e.g. through torch.distributed).  Each rank then passes the

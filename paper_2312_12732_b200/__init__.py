@@ -39,14 +39,15 @@ OUT_ROOT, OUT_ALL = 0, 1
 
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
-           "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version")
+           "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read")
 
 
 class mf_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("leaf", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
                 ("shard_count", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
-                ("input_mode", ctypes.c_int32), ("output_mode", ctypes.c_int32)]
+                ("input_mode", ctypes.c_int32), ("output_mode", ctypes.c_int32),
+                ("profile", ctypes.c_int32)]
 
 
 _P, _D, _I32, _I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64
@@ -64,6 +65,7 @@ _lib.mf_plan_products.argtypes = [_P] * 7
 _lib.mf_premix.argtypes = [_P, _I32, _P, _I64, _P, _P]
 _lib.mf_leaf.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _P, _P]
 _lib.mf_postmix.argtypes = [_P, _D, _P, _P, _I64, _P]
+_lib.mf_profile_read.argtypes = [_P, _P, ctypes.POINTER(_I32), _I32]
 _lib.mf_nccl_unique_id.argtypes = [_P]
 _lib.mf_nccl_comm_create.argtypes = [ctypes.POINTER(_P), _P, _I32, _I32]
 _lib.mf_nccl_comm_destroy.argtypes = [_P]
@@ -110,7 +112,8 @@ class Plan:
 
     def __init__(self, triple: triples.Triple | None, levels: int, n: int, *, leaf: str = "dmma",
                  device: int | None = None, shard_rank: int = 0, shard_count: int = 1,
-                 nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT):
+                 nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT,
+                 profile: bool = False):
         self.triple, self.levels, self.n = triple, int(levels), int(n)
         opt = mf_options()
         opt.struct_size = ctypes.sizeof(mf_options)
@@ -119,6 +122,7 @@ class Plan:
         opt.shard_rank, opt.shard_count = int(shard_rank), int(shard_count)
         opt.nccl_comm = nccl_comm.value if isinstance(nccl_comm, ctypes.c_void_p) else nccl_comm
         opt.input_mode, opt.output_mode = int(input_mode), int(output_mode)
+        opt.profile = int(bool(profile))
         self._opt = opt
         h = ctypes.c_void_p()
         if triple is None:
@@ -149,6 +153,17 @@ class Plan:
         _check(_lib.mf_plan_products(self._h, *[arrs[k].ctypes.data for k in
                                                 ("a_src", "a_idx", "b_src", "b_idx", "sign", "shard")]))
         return arrs
+
+    PHASES = ("premix_a", "premix_b", "leaf", "postmix", "comm")
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """Summed device ms per phase over the profiled mf_dgemm calls (mf_profile_read)."""
+        ms = (ctypes.c_double * 5)()
+        calls = _I32()
+        _check(_lib.mf_profile_read(self._h, ms, ctypes.byref(calls), int(reset)))
+        out = dict(zip(self.PHASES, list(ms)))
+        out["calls"] = calls.value
+        return out
 
     # -- the hot path ------------------------------------------------------------
     def dgemm(self, A, B, C=None, alpha: float = 1.0, stream=None):

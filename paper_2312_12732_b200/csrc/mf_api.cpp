@@ -201,6 +201,20 @@ void free_plan(Plan* pl) {
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
+  for (auto& set : pl->prof_events)
+    for (cudaEvent_t e : set) cudaEventDestroy(e);
+}
+
+// Events of the current call when profiling is on (nullptr otherwise).
+cudaEvent_t* prof_slot(Plan* pl) {
+  if (!pl->opt.profile) return nullptr;
+  if (pl->prof_used == pl->prof_events.size()) {
+    std::vector<cudaEvent_t> set(6, nullptr);
+    for (auto& e : set)
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    pl->prof_events.push_back(set);
+  }
+  return pl->prof_events[pl->prof_used++].data();
 }
 
 bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t n) {
@@ -480,18 +494,27 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
     A = pl->hA; lda = n; B = pl->hB; ldb = n;
   }
 
+  cudaEvent_t* ev = prof_slot(pl);
+  auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
+  mark(0);
   if (pl->levels == 0) {
+    mark(1); mark(2);
     if ((st = run_leaf(*pl, A, lda, B, ldb, nullptr, nullptr, C, ldc, 0, alpha, s)) != MF_OK) return st;
+    mark(3);
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
     MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
+    mark(1);
     MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
+    mark(2);
     // a3: all leaf products in one launch (K5)
     if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) != MF_OK)
       return st;
+    mark(3);
     // a4: fused post-addition (K6)
     MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
   }
+  mark(4);
   if (pl->nccl_comm) {
     // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
     ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
@@ -501,6 +524,29 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
                          : nc->Reduce(C, C, (size_t)n * n, ncclDouble, ncclSum, 0, comm, s);
     if (r != ncclSuccess) return nccl_fail(nc, r, "ncclReduce(C)");
   }
+  mark(5);
+  return MF_OK;
+}
+
+mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t reset) {
+  g_err.clear();
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (!pl->opt.profile) return fail(MF_ERR_INVALID_ARG, "plan was created without profile = 1");
+  DeviceGuard guard(pl->device);
+  double sum[5] = {0, 0, 0, 0, 0};
+  for (size_t c = 0; c < pl->prof_used; ++c) {
+    auto& ev = pl->prof_events[c];
+    MF_CUDA(cudaEventSynchronize(ev[5]), "cudaEventSynchronize");
+    for (int i = 0; i < 5; ++i) {
+      float t = 0.f;
+      MF_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]), "cudaEventElapsedTime");
+      sum[i] += t;
+    }
+  }
+  if (ms)
+    for (int i = 0; i < 5; ++i) ms[i] = sum[i];
+  if (calls) *calls = (int32_t)pl->prof_used;
+  if (reset) pl->prof_used = 0;
   return MF_OK;
 }
 

@@ -75,6 +75,9 @@ struct Plan {
   // NCCL
   void* nccl_comm = nullptr;
   cudaEvent_t done = nullptr;
+  // phase profiling (mf_options.profile): 6 events per mf_dgemm call
+  std::vector<std::vector<cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
 };
 
 // ---- launchers (mf_mix.cu, mf_leaf.cu); return cudaError_t of the launch ----
