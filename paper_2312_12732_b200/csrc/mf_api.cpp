@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -179,16 +180,39 @@ void kron(int po, int64_t Ro, const std::vector<double>& Uo, const std::vector<d
     }
 }
 
-mf_status upload_table(MixTable& t, bool with_slots) {
-  size_t bytes = sizeof(double) * t.coef.size() + (with_slots ? sizeof(int32_t) * t.out_map.size() : 0);
+// Device table: MixRow[nout] then MixTerm[...] -- each output's nonzero
+// terms in ascending input order (the oracle's combination order).
+mf_status upload_table(MixTable& t) {
+  std::vector<MixRow> rows;
+  std::vector<MixTerm> terms;
+  for (int o = 0; o < t.nout; ++o) {
+    MixRow r{};
+    r.first = (int32_t)terms.size();
+    r.target = t.out_map[o];
+    for (int k = 0; k < t.nin; ++k) {
+      const double v = t.coef[(size_t)o * t.nin + k];
+      if (v == 0.0) continue;
+      MixTerm term{};
+      term.src = k;
+      term.kind = v == 1.0 ? MIX_POS : (v == -1.0 ? MIX_NEG : MIX_GEN);
+      term.coef = v;
+      terms.push_back(term);
+    }
+    r.count = (int32_t)terms.size() - r.first;
+    rows.push_back(r);
+  }
+  t.nrow = (int)rows.size();
+  t.nterm = (int)terms.size();
+  const size_t bytes = sizeof(MixRow) * rows.size() + sizeof(MixTerm) * terms.size();
   if (bytes == 0) return MF_OK;
-  MF_CUDA(cudaMalloc(&t.d_coef, bytes), "cudaMalloc(coefficient table)");
-  std::vector<uint8_t> host(bytes);
-  memcpy(host.data(), t.coef.data(), sizeof(double) * t.coef.size());
-  if (with_slots)
-    memcpy(host.data() + sizeof(double) * t.coef.size(), t.out_map.data(),
-           sizeof(int32_t) * t.out_map.size());
-  MF_CUDA(cudaMemcpy(t.d_coef, host.data(), bytes, cudaMemcpyHostToDevice), "upload table");
+  if (bytes > 200 * 1024) return fail(MF_ERR_UNSUPPORTED, "mix table of %zu bytes exceeds shared memory", bytes);
+  MF_CUDA(cudaMalloc(&t.d_table, bytes), "cudaMalloc(coefficient table)");
+  MF_CUDA(cudaMemcpy(t.d_table, rows.data(), sizeof(MixRow) * rows.size(), cudaMemcpyHostToDevice),
+          "upload table");
+  if (!terms.empty())
+    MF_CUDA(cudaMemcpy(static_cast<uint8_t*>(t.d_table) + sizeof(MixRow) * rows.size(), terms.data(),
+                       sizeof(MixTerm) * terms.size(), cudaMemcpyHostToDevice),
+            "upload table");
   return MF_OK;
 }
 
@@ -196,8 +220,8 @@ void free_plan(Plan* pl) {
   if (!pl) return;
   DeviceGuard g(pl->device);
   cudaDeviceSynchronize();
-  for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_coef,
-                  (void*)pl->mixB.d_coef, (void*)pl->mixC.d_coef, (void*)pl->hA, (void*)pl->hB,
+  for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_table,
+                  (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
@@ -281,10 +305,9 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     P *= p;
     RL *= R;
   }
-  if (P > 9) return fail(MF_ERR_UNSUPPORTED, "flattened split factor p^levels = %lld > 9", (long long)P);
-  if (P * P * RL > 28000)
-    return fail(MF_ERR_UNSUPPORTED, "flattened triple too large for the post-add table (%lld x %lld)",
-                (long long)(P * P), (long long)RL);
+  if (P > 256 || RL > (1 << 20))
+    return fail(MF_ERR_UNSUPPORTED, "flattened triple too large (p^levels = %lld, R^levels = %lld)",
+                (long long)P, (long long)RL);
   if (shard_count > RL)
     return fail(MF_ERR_INVALID_ARG, "shard_count %d exceeds the %lld leaf products", shard_count,
                 (long long)RL);
@@ -347,6 +370,9 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
   for (int64_t q = 0; q < RL; ++q)
     if (pl->prods[q].shard == pl->shard_rank) pl->my_prods.push_back((int32_t)q);
 
+  // unsharded plans of a compiled-in triple use the specialised K4/K6
+  if (levels > 0 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) pl->fixed_id = fixed_match(*pl);
+
   // ---- mix tables for this shard ----
   for (int side = 0; side < 2 && levels > 0; ++side) {
     MixTable& t = side == 0 ? pl->mixA : pl->mixB;
@@ -365,6 +391,7 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     c.nin = (int)RL;
     c.nout = NB;
     c.coef.assign((size_t)NB * RL, 0.0);
+    for (int i = 0; i < NB; ++i) c.out_map.push_back(i);
     for (int32_t q : pl->my_prods)
       for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
   }
@@ -379,9 +406,8 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     if (cudaMalloc(&pl->Pw, pb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace P (%zu bytes)", pb); }
     pl->ws_bytes = tb + sb + pb;
     mf_status st;
-    if ((st = upload_table(pl->mixA, true)) != MF_OK ||
-        (st = upload_table(pl->mixB, true)) != MF_OK ||
-        (st = upload_table(pl->mixC, false)) != MF_OK) {
+    if ((st = upload_table(pl->mixA)) != MF_OK || (st = upload_table(pl->mixB)) != MF_OK ||
+        (st = upload_table(pl->mixC)) != MF_OK) {
       free_plan(pl.get());
       return st;
     }

@@ -1,0 +1,355 @@
+// mf_fixed.cu -- K4/K6 specialised at compile time for the catalog triples.
+//
+// For a triple known when the library is built (Strassen-Winograd, the
+// paper's DeepMind-format Strassen, Strassen 1969, Laderman, and the
+// Kronecker squares of the 2x2 ones -- PAPER.md L303-313), the coefficient
+// pattern of Eq. "strassen" is a compile-time constant: C++17 constexpr
+// evaluation computes the Kronecker flattening, the alias classification and
+// the slot numbering (the same rules mf_plan applies at run time), and fold
+// expressions expand every combination into straight-line code -- no
+// coefficient loads, no branches, +-1 terms as single (negated) adds.  The
+// plan selects these kernels when its flattened triple equals one of them
+// exactly; anything else runs the generic table-driven kernels of mf_mix.cu.
+//
+// Summation order is the oracle's (ascending input index, accumulator
+// starting at -0.0, which is bitwise the first-term rule; R7/R8).
+#include <cstdint>
+#include <utility>
+
+#include "mf_internal.h"
+
+namespace mf {
+namespace fixed {
+
+template <int NB, int R>
+struct Tri {
+  int8_t U[NB][R], V[NB][R], W[NB][R];
+};
+
+// Blocks 0=(1,1) 1=(1,2) 2=(2,1) 3=(2,2); W rows in natural C order.
+inline constexpr Tri<4, 7> kSW = {
+    {{1, 0, 1, 0, 0, -1, 1}, {0, 1, 1, 0, 0, 0, 0}, {0, 0, -1, 0, 1, 1, -1}, {0, 0, -1, 1, 1, 1, 0}},
+    {{1, 0, 0, 1, -1, 1, 0}, {0, 0, 0, -1, 1, -1, -1}, {0, 1, 0, -1, 0, 0, 0}, {0, 0, 1, 1, 0, 1, 1}},
+    {{1, 1, 0, 0, 0, 0, 0}, {1, 0, 1, 0, 1, 1, 0}, {1, 0, 0, -1, 0, 1, 1}, {1, 0, 0, 0, 1, 1, 1}}};
+inline constexpr Tri<4, 7> kPS = {
+    {{0, 1, 1, 0, 1, 1, 0}, {0, 0, -1, 1, 0, 0, 0}, {1, 1, 1, 0, 1, 0, 0}, {-1, -1, -1, 0, 0, 0, 1}},
+    {{0, 0, 0, 0, 1, 1, 0}, {1, 1, 0, 0, 1, 0, 1}, {0, 1, 1, 1, 1, 0, 0}, {0, 1, 1, 0, 1, 0, 1}},
+    {{0, 0, 0, 1, 0, 1, 0}, {-1, 1, -1, -1, 0, 0, 0}, {0, -1, 0, 0, 1, -1, -1}, {1, 0, 0, 0, 0, 0, 1}}};
+inline constexpr Tri<4, 7> kS69 = {
+    {{1, 0, 1, 0, 1, -1, 0}, {0, 0, 0, 0, 1, 0, 1}, {0, 1, 0, 0, 0, 1, 0}, {1, 1, 0, 1, 0, 0, -1}},
+    {{1, 1, 0, -1, 0, 1, 0}, {0, 0, 1, 0, 0, 1, 0}, {0, 0, 0, 1, 0, 0, 1}, {1, 0, -1, 0, 1, 0, 1}},
+    {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0}, {0, 1, 0, 1, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0}}};
+// Laderman 1976, blocks 0..8 row-major over the 3x3 grid.
+inline constexpr Tri<9, 23> kLD = {
+    {{1, 1, 0, -1, 0, 1, -1, -1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
+     {1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, -1, 1, 1, 0, -1, 1, 0, 0, 0, 0, 0, 0},
+     {-1, -1, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0},
+     {-1, 0, 1, 1, 1, 0, 0, 0, 0, -1, 0, 0, 0, 0, 0, 1, 0, 1, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0, -1, 0, 0, 0, 0, 0, 1, -1, 1, 0, 1, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 1, 1, 1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},
+     {-1, 0, 0, 0, 0, 0, 1, 0, 1, -1, 1, 1, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0},
+     {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1}},
+    {{0, 0, -1, 1, -1, 1, 1, 0, -1, 0, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, -1, 1, -1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},
+     {0, 0, 0, 0, 0, 0, -1, 1, 1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0},
+     {0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
+     {1, 1, -1, 1, 0, 0, 0, 0, 0, 0, -1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, -1, 0, 0, 0, 1, -1, 0, 1, -1, 0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0},
+     {0, 0, -1, 0, 0, 0, 0, 0, 0, 0, -1, 1, 0, 1, -1, 1, 0, -1, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, -1, -1, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0},
+     {0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1, -1, 1, 0, 0, 0, 0, 1}},
+    {{0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0},
+     {1, 0, 0, 1, 1, 1, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 1, 1, 0, 1, 1, 0, 0, 0, 1, 0, 1, 0, 1, 0, 0, 0, 0, 0},
+     {0, 1, 1, 1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 0, 0, 0, 0},
+     {0, 1, 0, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 1, 0, 0, 1, 0, 0},
+     {0, 0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 1, 0},
+     {0, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1}}};
+
+// PAPER.md L303-309 with SPEC.md L244's row interleave; q = qo*Ri + qi.
+template <int Po, int NBo, int Ro, int Pi, int NBi, int Ri>
+constexpr Tri<NBo * NBi, Ro * Ri> kron(const Tri<NBo, Ro>& o, const Tri<NBi, Ri>& in) {
+  Tri<NBo * NBi, Ro * Ri> t{};
+  constexpr int P = Po * Pi;
+  for (int b = 0; b < NBo; ++b)
+    for (int s = 0; s < NBi; ++s) {
+      const int row = ((b / Po) * Pi + s / Pi) * P + (b % Po) * Pi + s % Pi;
+      for (int qo = 0; qo < Ro; ++qo)
+        for (int qi = 0; qi < Ri; ++qi) {
+          const int q = qo * Ri + qi;
+          t.U[row][q] = (int8_t)(o.U[b][qo] * in.U[s][qi]);
+          t.V[row][q] = (int8_t)(o.V[b][qo] * in.V[s][qi]);
+          t.W[row][q] = (int8_t)(o.W[b][qo] * in.W[s][qi]);
+        }
+    }
+  return t;
+}
+
+inline constexpr Tri<16, 49> kSW2 = kron<2, 4, 7, 2, 4, 7>(kSW, kSW);
+inline constexpr Tri<16, 49> kPS2 = kron<2, 4, 7, 2, 4, 7>(kPS, kPS);
+inline constexpr Tri<16, 49> kS692 = kron<2, 4, 7, 2, 4, 7>(kS69, kS69);
+
+// Kernel templates are parameterised by a tag TYPE (nvcc's host stubs cannot
+// name reference template arguments); device helpers take the reference.
+struct TagSW { static constexpr const auto& T = kSW; };
+struct TagPS { static constexpr const auto& T = kPS; };
+struct TagS69 { static constexpr const auto& T = kS69; };
+struct TagLD { static constexpr const auto& T = kLD; };
+struct TagSW2 { static constexpr const auto& T = kSW2; };
+struct TagPS2 { static constexpr const auto& T = kPS2; };
+struct TagS692 { static constexpr const auto& T = kS692; };
+
+// ---- compile-time classification (the rule of mf_plan step 5) ----
+template <int NB, int R>
+constexpr int nnz_col(const int8_t (&M)[NB][R], int q) {
+  int c = 0;
+  for (int k = 0; k < NB; ++k) c += M[k][q] != 0;
+  return c;
+}
+template <int NB, int R>
+constexpr bool is_alias(const int8_t (&M)[NB][R], int q) {
+  if (nnz_col(M, q) != 1) return false;
+  for (int k = 0; k < NB; ++k)
+    if (M[k][q] != 0) return M[k][q] == 1 || M[k][q] == -1;
+  return false;
+}
+template <int NB, int R>
+constexpr int alias_sign(const int8_t (&M)[NB][R], int q) {
+  if (!is_alias(M, q)) return 1;
+  for (int k = 0; k < NB; ++k)
+    if (M[k][q] != 0) return M[k][q];
+  return 1;
+}
+template <int NB, int R>
+constexpr int slot_of(const int8_t (&M)[NB][R], int q) {  // index among materialised columns
+  int s = 0;
+  for (int j = 0; j < q; ++j) s += !is_alias(M, j);
+  return s;
+}
+
+// Scalar views of the compile-time tables (constexpr scalars are usable in
+// device code; the arrays themselves stay host-side).
+template <const auto& T, int SIDE, int K, int Q>
+inline constexpr int coef_v = SIDE == 0 ? T.U[K][Q] : (SIDE == 1 ? T.V[K][Q] : T.W[K][Q]);
+template <const auto& T, int SIDE, int Q>
+inline constexpr bool alias_v = is_alias(SIDE == 0 ? T.U : T.V, Q);
+template <const auto& T, int SIDE, int Q>
+inline constexpr int slot_v = slot_of(SIDE == 0 ? T.U : T.V, Q);
+template <const auto& T, int Q>
+inline constexpr int sign_v = alias_sign(T.U, Q) * alias_sign(T.V, Q);
+
+template <int VW> struct V { double v[VW]; };
+
+template <int VW>
+__device__ __forceinline__ V<VW> ld_stream(const double* p) {
+  V<VW> r;
+  if constexpr (VW == 4) {
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  } else if constexpr (VW == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  } else {
+    r.v[0] = __ldg(p);
+  }
+  return r;
+}
+
+template <int VW>
+__device__ __forceinline__ void st_vec(double* p, const V<VW>& x) {
+  if constexpr (VW == 4) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(x.v[0]), "d"(x.v[1]), "d"(x.v[2]), "d"(x.v[3]) : "memory");
+  } else if constexpr (VW == 2) {
+    asm volatile("st.global.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(x.v[0]), "d"(x.v[1]) : "memory");
+  } else {
+    p[0] = x.v[0];
+  }
+}
+
+template <int C, int VW>
+__device__ __forceinline__ void acc_term(V<VW>& acc, const V<VW>& x) {
+  if constexpr (C == 1) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc.v[e] = __dadd_rn(acc.v[e], x.v[e]);
+  } else if constexpr (C == -1) {
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc.v[e] = __dadd_rn(acc.v[e], -x.v[e]);
+  }
+}
+
+// ---- K4: T slots (SIDE 0, from U) or S slots (SIDE 1, from V) ----
+template <const auto& T, int SIDE, int P, int VW, int Q, int... Ks>
+__device__ __forceinline__ void premix_one(const V<VW> (&x)[P * P], double* out, int64_t off,
+                                           int64_t mm, std::integer_sequence<int, Ks...>) {
+  if constexpr (!alias_v<T, SIDE, Q>) {
+    V<VW> acc;
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc.v[e] = -0.0;
+    (acc_term<coef_v<T, SIDE, Ks, Q>, VW>(acc, x[Ks]), ...);
+    st_vec<VW>(out + (int64_t)slot_v<T, SIDE, Q> * mm + off, acc);
+  }
+}
+
+template <const auto& T, int SIDE, int P, int VW, int... Qs>
+__device__ __forceinline__ void premix_all(const V<VW> (&x)[P * P], double* out, int64_t off,
+                                           int64_t mm, std::integer_sequence<int, Qs...>) {
+  (premix_one<T, SIDE, P, VW, Qs>(x, out, off, mm, std::make_integer_sequence<int, P * P>{}), ...);
+}
+
+template <class Tag, int SIDE, int P, int R, int VW>
+__global__ void __launch_bounds__(256) premix_fixed(const double* __restrict__ X, int64_t ldx,
+                                                    int64_t m, double* __restrict__ out) {
+  constexpr int NB = P * P;
+  const int64_t vpr = m / VW;
+  const int64_t total = m * vpr;
+  const int64_t mm = m * m;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / vpr;
+    const int64_t c = (idx - r * vpr) * VW;
+    V<VW> x[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) x[k] = ld_stream<VW>(X + ((k / P) * m + r) * ldx + (k % P) * m + c);
+    premix_all<Tag::T, SIDE, P, VW>(x, out, r * m + c, mm, std::make_integer_sequence<int, R>{});
+  }
+}
+
+// ---- K6: C_i = alpha * sum_q W[i][q] * sign_q * P_q' ----
+template <const auto& T, int P, int VW, int Q, int... Is>
+__device__ __forceinline__ void postmix_one(V<VW> (&acc)[P * P], const double* __restrict__ Pw,
+                                            int64_t off, int64_t mm,
+                                            std::integer_sequence<int, Is...>) {
+  constexpr int nz = (0 + ... + (coef_v<T, 2, Is, Q> != 0));
+  if constexpr (nz > 0) {
+    const V<VW> x = ld_stream<VW>(Pw + (int64_t)Q * mm + off);
+    (acc_term<coef_v<T, 2, Is, Q> * sign_v<T, Q>, VW>(acc[Is], x), ...);
+  }
+}
+
+template <const auto& T, int P, int VW, int... Qs>
+__device__ __forceinline__ void postmix_all(V<VW> (&acc)[P * P], const double* __restrict__ Pw,
+                                            int64_t off, int64_t mm,
+                                            std::integer_sequence<int, Qs...>) {
+  (postmix_one<T, P, VW, Qs>(acc, Pw, off, mm, std::make_integer_sequence<int, P * P>{}), ...);
+}
+
+template <class Tag, int P, int R, int VW>
+__global__ void __launch_bounds__(256) postmix_fixed(const double* __restrict__ Pw, int64_t m,
+                                                     double alpha, double* __restrict__ C,
+                                                     int64_t ldc) {
+  constexpr int NB = P * P;
+  const int64_t vpr = m / VW;
+  const int64_t total = m * vpr;
+  const int64_t mm = m * m;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / vpr;
+    const int64_t c = (idx - r * vpr) * VW;
+    V<VW> acc[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+      for (int e = 0; e < VW; ++e) acc[i].v[e] = -0.0;
+    postmix_all<Tag::T, P, VW>(acc, Pw, r * m + c, mm, std::make_integer_sequence<int, R>{});
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (alpha != 1.0) {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc[i].v[e] = __dmul_rn(alpha, acc[i].v[e]);
+      }
+      st_vec<VW>(C + ((i / P) * m + r) * ldc + (i % P) * m + c, acc[i]);
+    }
+  }
+}
+
+int grid_for(int64_t work) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (work + 255) / 256;
+  const int64_t cap = (int64_t)sms * 8;
+  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
+}
+
+template <int NB, int R>
+bool equal(const Tri<NB, R>& t, const Plan& pl) {
+  if ((int64_t)NB != (int64_t)pl.P * pl.P || (int64_t)R != pl.RL) return false;
+  for (int k = 0; k < NB; ++k)
+    for (int q = 0; q < R; ++q)
+      if (pl.U[(size_t)k * R + q] != t.U[k][q] || pl.V[(size_t)k * R + q] != t.V[k][q] ||
+          pl.W[(size_t)k * R + q] != t.W[k][q])
+        return false;
+  return true;
+}
+
+template <class Tag, int P, int R, int VW>
+cudaError_t run_premix(int side, const double* X, int64_t ldx, int64_t m, double* out,
+                       cudaStream_t s) {
+  const int grid = grid_for(m * (m / VW));
+  if (side == 0) premix_fixed<Tag, 0, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out);
+  else premix_fixed<Tag, 1, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out);
+  return cudaGetLastError();
+}
+
+template <class Tag, int P, int R, int VW>
+cudaError_t run_postmix(const double* Pw, int64_t m, double alpha, double* C, int64_t ldc,
+                        cudaStream_t s) {
+  postmix_fixed<Tag, P, R, VW><<<grid_for(m * (m / VW)), 256, 0, s>>>(Pw, m, alpha, C, ldc);
+  return cudaGetLastError();
+}
+
+bool al(const void* p, int b) { return (reinterpret_cast<uintptr_t>(p) % b) == 0; }
+
+}  // namespace fixed
+
+// Identify the plan's flattened triple among the compiled-in ones (exact
+// coefficient equality).  Returns an id >= 1, or 0 (generic kernels).
+int fixed_match(const Plan& pl) {
+  using namespace fixed;
+  if (equal(kSW, pl)) return 1;
+  if (equal(kPS, pl)) return 2;
+  if (equal(kS69, pl)) return 3;
+  if (equal(kLD, pl)) return 4;
+  if (equal(kSW2, pl)) return 5;
+  if (equal(kPS2, pl)) return 6;
+  if (equal(kS692, pl)) return 7;
+  return 0;
+}
+
+#define MF_FIXED_SWITCH(ID, CALL)                     \
+  switch (ID) {                                       \
+    case 1: return CALL(fixed::TagSW, 2, 7);          \
+    case 2: return CALL(fixed::TagPS, 2, 7);          \
+    case 3: return CALL(fixed::TagS69, 2, 7);         \
+    case 4: return CALL(fixed::TagLD, 3, 23);         \
+    case 5: return CALL(fixed::TagSW2, 4, 49);        \
+    case 6: return CALL(fixed::TagPS2, 4, 49);        \
+    case 7: return CALL(fixed::TagS692, 4, 49);       \
+    default: return cudaErrorInvalidValue;            \
+  }
+
+// 256-bit path only (the bench/production shapes); callers fall back to the
+// generic kernels when fixed_vw4_ok() is false.
+bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t ldb) {
+  return m % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0 && fixed::al(a, 32) && fixed::al(b, 32);
+}
+
+cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
+                                double* out, cudaStream_t s) {
+#define PRE(T_, P_, R_) fixed::run_premix<T_, P_, R_, 4>(side, X, ldx, m, out, s)
+  MF_FIXED_SWITCH(id, PRE)
+#undef PRE
+}
+
+cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
+                                 int64_t ldc, cudaStream_t s) {
+#define POST(T_, P_, R_) fixed::run_postmix<T_, P_, R_, (P_ >= 4 ? 2 : 4)>(Pw, m, alpha, C, ldc, s)
+  MF_FIXED_SWITCH(id, POST)
+#undef POST
+}
+
+}  // namespace mf

@@ -38,11 +38,26 @@ struct LeafJob {
 
 // Coefficient table of one mix kernel launch: nout outputs, each a
 // combination of up to nin inputs, coef[o * nin + k] (0 = absent).
+// Device form: MixRow[nrow] then MixTerm[nterm]; row o's terms are
+// terms[first .. first+count) in ascending input order (the oracle's order).
+enum MixKind : int32_t { MIX_POS = 0, MIX_NEG = 1, MIX_GEN = 2 };
+struct MixRow {
+  int32_t first, count;
+  int32_t target;  // output block / slot id in the output view
+  int32_t pad;
+};
+struct MixTerm {
+  int32_t src;   // input block / slot id in the input view
+  int32_t kind;  // MixKind
+  double coef;   // used when kind == MIX_GEN
+};
+
 struct MixTable {
   int nin = 0, nout = 0;
   std::vector<double> coef;      // nout x nin
   std::vector<int32_t> out_map;  // output o -> slot / C block it writes
-  double* d_coef = nullptr;      // device copy (owned by the plan)
+  int nrow = 0, nterm = 0;       // device table sizes
+  void* d_table = nullptr;       // device MixRow + MixTerm table (owned by the plan)
 };
 
 struct Plan {
@@ -58,6 +73,7 @@ struct Plan {
   std::vector<int32_t> mat_a_col, mat_b_col;  // slot -> product column q
   mf_options opt{};
   int leaf = MF_LEAF_DMMA;
+  int fixed_id = 0;  // > 0: compile-time specialised K4/K6 (mf_fixed.cu) for this triple
   int shard_rank = 0, shard_count = 1;
   // shard-local view: the products this plan's rank computes
   std::vector<int32_t> my_prods;  // product indices q
@@ -101,6 +117,14 @@ struct LeafArgs {
   const LeafJob* jobs; int n_jobs;
 };
 bool leaf_tma_supported(const LeafArgs& a);
+
+// mf_fixed.cu: compile-time specialised K4/K6 for the catalog triples
+int fixed_match(const Plan& pl);
+bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t ldb);
+cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
+                                double* out, cudaStream_t s);
+cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
+                                 int64_t ldc, cudaStream_t s);
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s);
 
 }  // namespace mf

@@ -17,18 +17,25 @@
 //    neighbouring block); a materialised operand is a slot of the T/S
 //    workspace (3-D map {col, row, slot}).
 //  * CTA tile 128x128x16.  Each MMA warp owns 64x32 of C: 64 fp64
-//    accumulators per thread.  Fragments are fetched with 128-bit LDS:
-//      A (SWIZZLE_128B, rows of 16 k): lane (r=L/4, kk=L%4) loads
-//        A[r][2kk], A[r][2kk+1] -> the k-permutation k = 8g + 2kk + s feeds
-//        two k-steps s = 0,1 (conflict-free: 4 wavefronts per 512 B);
-//      B (no swizzle, rows of 128 n): lane (kk=L%4, nn=L/4) loads
-//        B[8g+2kk+s][2nn], B[..][2nn+1] -> the n-permutation n = 2c + j feeds
-//        two n-subtiles j = 0,1; each thread then owns 4 CONSECUTIVE output
-//        columns, stored with one 256-bit st.global.v4.f64.
+//    accumulators per thread.  Fragments are fetched with 128-bit LDS, which
+//    shared memory serves per quarter-warp (8 lanes): conflict-free needs the
+//    8 lanes of a quarter to hit 8 distinct 16-byte bank groups.
+//      Both tiles are TMA-written with SWIZZLE_128B in rows of 16 doubles
+//      (A: [128 m][16 k]; B: 8 boxes of [16 k][16 n]); physical 16-byte chunk
+//      = logical chunk ^ (row & 7).
+//      A: lane (r=L/4, kk=L%4) loads the k-pair chunk c(kk,g) of row r;
+//      B: lane (kk, nn=L/4) loads B[2c(kk,g)+s][2nn], B[..][2nn+1] (n-pair).
+//      The k-permutation k = 2c(kk,g) + s with c(.,0) = {0,3,5,6},
+//      c(.,1) = {1,2,4,7} makes both conflict-free: A needs one chunk of
+//      every pair {2j,2j+1} (rows 2q, 2q+1 share a quarter), B needs c mod 4
+//      distinct (its four k rows must land on four different XOR masks).
+//      Each k-step s feeds one DMMA; the n-permutation n = 2c + j of B makes
+//      each thread own 4 CONSECUTIVE output columns (one 256-bit store).
 //  * Grid = products x tiles, 1 CTA/SM (256 threads, ~164 KB smem); tiles of
 //    a product are rasterised in groups of 8 tile-rows for L2 reuse.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "mf_internal.h"
@@ -46,9 +53,17 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
 constexpr int GROUP_M = 8;
 
+// B-tile staging modes (all TMA):
+//   B_ROWS:  one box [16 k][128 n], no swizzle (1 KB rows; LDS.128 4-way conflicted)
+//   B_BOXES: 8 boxes [16 k][16 n], SWIZZLE_128B (conflict-free, 8 TMA issues)
+//   B_5D:    one 5-D box {16 n, 16 k, 8 n-blocks} giving the B_BOXES layout with
+//            one TMA issue (needs m % 16 == 0)
+enum BMode : int { B_ROWS = 0, B_BOXES = 1, B_5D = 2 };
+
 struct LeafParams {
   int64_t m;
   int tiles_m, tiles_n, kblocks;
+  int bmode;
   double* out;
   int64_t ldo, out_stride;
   double alpha;
@@ -99,6 +114,16 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3, %4, %5}], [%6];"
       :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
          "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+         "r"(c4), "r"(bar)
       : "memory");
 }
 
@@ -158,8 +183,19 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t dA = s_base + s * STAGE_BYTES, dB = dA + A_BYTES;
     if (a_ws) tma_load_3d(dA, mapA, fb, kb * BK, tm * BM, job.a_coord);
     else      tma_load_4d(dA, mapA, fb, kb * BK, a_bc, tm * BM, a_br);
-    if (b_ws) tma_load_3d(dB, mapB, fb, tn * BN, kb * BK, job.b_coord);
-    else      tma_load_4d(dB, mapB, fb, tn * BN, b_bc, kb * BK, b_br);
+    if (prm.bmode == B_BOXES) {
+#pragma unroll
+      for (int j = 0; j < BN / 16; ++j) {
+        if (b_ws) tma_load_3d(dB + j * 2048, mapB, fb, tn * BN + 16 * j, kb * BK, job.b_coord);
+        else      tma_load_4d(dB + j * 2048, mapB, fb, tn * BN + 16 * j, b_bc, kb * BK, b_br);
+      }
+    } else if (prm.bmode == B_5D) {
+      if (b_ws) tma_load_4d(dB, mapB, fb, 0, kb * BK, tn * (BN / 16), job.b_coord);
+      else      tma_load_5d(dB, mapB, fb, 0, kb * BK, tn * (BN / 16), b_bc, b_br);
+    } else {
+      if (b_ws) tma_load_3d(dB, mapB, fb, tn * BN, kb * BK, job.b_coord);
+      else      tma_load_4d(dB, mapB, fb, tn * BN, b_bc, kb * BK, b_br);
+    }
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapA)) : "memory");
@@ -180,12 +216,26 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
       for (int u = 0; u < 2; ++u) { acc[i][j][u][0] = 0.0; acc[i][j][u][1] = 0.0; }
 
-  // per-lane shared-memory offsets (bytes) inside a stage
-  uint32_t offA[2];
+  // per-lane shared-memory offsets (bytes) inside a stage; see the header
+  // for the k-permutation c(kk, g) that makes every LDS.128 conflict-free.
+  const uint32_t c0 = (0x6530u >> (4 * lk)) & 0xf;  // c(kk, 0) in {0,3,5,6}
+  const uint32_t c1 = (0x7421u >> (4 * lk)) & 0xf;  // c(kk, 1) in {1,2,4,7}
+  uint32_t offA[2], offB[2][2];
+  offA[0] = (wm * 64 + lr) * 128 + ((c0 ^ lr) << 4);
+  offA[1] = (wm * 64 + lr) * 128 + ((c1 ^ lr) << 4);
+  uint32_t nj_stride;
 #pragma unroll
-  for (int g = 0; g < 2; ++g)
-    offA[g] = (wm * 64 + lr) * 128 + ((((4 * g + lk) ^ lr) & 7) << 4);
-  const uint32_t offB = (2 * lk) * (BN * 8) + (wn * 32 + 2 * lr) * 8;
+  for (int s2 = 0; s2 < 2; ++s2) {
+    const uint32_t r0 = 2 * c0 + s2, r1 = 2 * c1 + s2;  // B rows (k) for g = 0, 1
+    if (prm.bmode == B_ROWS) {
+      offB[0][s2] = r0 * (BN * 8) + (wn * 32 + 2 * lr) * 8;
+      offB[1][s2] = r1 * (BN * 8) + (wn * 32 + 2 * lr) * 8;
+    } else {
+      offB[0][s2] = (2 * wn) * 2048 + r0 * 128 + ((lr ^ (r0 & 7)) << 4);
+      offB[1][s2] = (2 * wn) * 2048 + r1 * 128 + ((lr ^ (r1 & 7)) << 4);
+    }
+  }
+  nj_stride = prm.bmode == B_ROWS ? 16 * 8 : 2048;
 
   for (int kb = 0; kb < prm.kblocks; ++kb) {
     if (warp == 0) {
@@ -200,7 +250,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t sA = s_base + s * STAGE_BYTES, sB = sA + A_BYTES;
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
-      double a[8][2];
+      double a[8][2];  // [mi][s]
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, a[mi][0], a[mi][1]);
       double b[2][2][2];  // [nj][s][j]
@@ -208,7 +258,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       for (int nj = 0; nj < 2; ++nj)
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2)
-          lds128(sB + offB + (8 * g + s2) * (BN * 8) + nj * 16 * 8, b[nj][s2][0], b[nj][s2][1]);
+          lds128(sB + offB[g][s2] + nj * nj_stride, b[nj][s2][0], b[nj][s2][1]);
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
@@ -332,6 +382,31 @@ bool encode_slot_view(CUtensorMap* map, const double* X, int slots, int64_t m, u
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 5-D view of B for B_5D: {n-in-16, row, n-block-of-16, block-col, block-row}
+// (or 4-D {n-in-16, row, n-block, slot} for a workspace); box {16, 16, 8, 1, 1}
+// lands in shared memory as 8 consecutive [16 k][16 n] sub-tiles.
+bool encode_b5d(CUtensorMap* map, const double* X, int64_t ld, int P, int64_t m, bool slots,
+                int n_slots) {
+  if (slots) {
+    cuuint64_t dims[4] = {16, (cuuint64_t)m, (cuuint64_t)(m / 16), (cuuint64_t)(n_slots > 0 ? n_slots : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)m * 8, 128, (cuuint64_t)m * m * 8};
+    cuuint32_t box[4] = {16, 16, 8, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims,
+                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+  }
+  cuuint64_t dims[5] = {16, (cuuint64_t)m, (cuuint64_t)(m / 16), (cuuint64_t)P, (cuuint64_t)P};
+  cuuint64_t strides[4] = {(cuuint64_t)ld * 8, 128, (cuuint64_t)m * 8, (cuuint64_t)m * ld * 8};
+  cuuint32_t box[5] = {16, 16, 8, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(X), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -348,13 +423,31 @@ bool leaf_tma_supported(const LeafArgs& a) {
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   if (a.n_jobs == 0 || a.m == 0) return cudaSuccess;
   if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a)) {
+    int bmode = B_ROWS;  // measured fastest (profiles/leaf_bmode_r01.json)
+    if (const char* e = getenv("MF_LEAF_BMODE")) bmode = atoi(e);  // experiments: 0, 1, 2
+    if (bmode == B_5D && a.m % 16 != 0) bmode = B_BOXES;
     CUtensorMap mA, mT, mB, mS;
     bool ok = encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              encode_block_view(&mB, a.B, a.ldb, a.P, a.m, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
               encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM,
-                               CU_TENSOR_MAP_SWIZZLE_128B) &&
-              encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, BN, BK,
-                               CU_TENSOR_MAP_SWIZZLE_NONE);
+                               CU_TENSOR_MAP_SWIZZLE_128B);
+    if (bmode == B_5D) {
+      ok = ok && encode_b5d(&mB, a.B, a.ldb, a.P, a.m, false, 0) &&
+           encode_b5d(&mS, a.S ? a.S : a.B, a.m, 1, a.m, true, a.n_slots_b);
+      if (!ok) {  // fall back to per-sub-tile boxes if the 5-D view is rejected
+        bmode = B_BOXES;
+        ok = encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+             encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM,
+                              CU_TENSOR_MAP_SWIZZLE_128B);
+      }
+    }
+    if (bmode == B_BOXES)
+      ok = ok && encode_block_view(&mB, a.B, a.ldb, a.P, a.m, 16, BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, 16, BK,
+                            CU_TENSOR_MAP_SWIZZLE_128B);
+    if (bmode == B_ROWS)
+      ok = ok && encode_block_view(&mB, a.B, a.ldb, a.P, a.m, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, BN, BK,
+                            CU_TENSOR_MAP_SWIZZLE_NONE);
     if (!ok) return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
@@ -368,6 +461,7 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.tiles_m = (int)((a.m + BM - 1) / BM);
     prm.tiles_n = (int)((a.m + BN - 1) / BN);
     prm.kblocks = (int)((a.m + BK - 1) / BK);
+    prm.bmode = bmode;
     prm.out = a.out;
     prm.ldo = a.ldo;
     prm.out_stride = a.out_block_stride;

@@ -3,16 +3,20 @@
 // Both are the linear-combination steps of Eq. "strassen":
 //   K4:  X_s = sum_k M[k][q_s] * Blk_k(X)      (T_q from A with U, S_q from B with V)
 //   K6:  C_i = alpha * sum_q W'[i][q] * P_q'     (W' = W with aliased signs folded in)
-// computed for ALL outputs of a level in ONE pass over HBM: each thread owns
-// one VW-wide vector position (r, c) inside an m x m block, loads that
-// position of every input block once (256-bit ld.global.nc.v4.f64 on
-// sm_100a), and writes that position of every output.  HBM-bound: the
-// algorithmic traffic is (#inputs read + #outputs written) * 8 * m^2 bytes.
+// computed for ALL outputs of a level in ONE launch: a CTA owns a segment of
+// positions and produces every output for it, so each input element comes
+// from HBM once (re-reads by other outputs hit L1) and each output is written
+// once (256-bit ld/st.global.v4.f64 on sm_100a).  HBM-bound: the algorithmic
+// traffic is (#inputs read + #outputs written) * 8 * m^2 bytes.
 //
 // Summation order is fixed -- first nonzero term c0*X_{k0}, then
 // acc = acc + c*X_k in ascending k (q for K6), separate multiply and add
 // (__dmul_rn/__dadd_rn, never contracted), alpha applied last -- the order
 // the oracle uses (reading R7/R8), so K4/K6 are bit-exact with it.
+// Coefficients arrive as warp-uniform term lists: +-1 terms cost one add.
+#include <algorithm>
+#include <cstdlib>
+
 #include "mf_internal.h"
 
 namespace mf {
@@ -20,14 +24,31 @@ namespace {
 
 template <int VW> struct Vec { double v[VW]; };
 
+// Streaming 256/128-bit loads that bypass L1 (inputs read exactly once).
 template <int VW>
-__device__ __forceinline__ Vec<VW> load_vec(const double* p) {
+__device__ __forceinline__ Vec<VW> load_stream(const double* p) {
   Vec<VW> r;
   if constexpr (VW == 4) {
     asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
   } else if constexpr (VW == 2) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  } else {
+    r.v[0] = __ldg(p);
+  }
+  return r;
+}
+
+// L1-allocating loads (inputs re-read by other warps of the CTA).
+template <int VW>
+__device__ __forceinline__ Vec<VW> load_vec(const double* p) {
+  Vec<VW> r;
+  if constexpr (VW == 4) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  } else if constexpr (VW == 2) {
+    asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];"
                  : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
   } else {
     r.v[0] = __ldg(p);
@@ -47,147 +68,121 @@ __device__ __forceinline__ void store_vec(double* p, const Vec<VW>& x) {
   }
 }
 
-// K4: pre-addition.  coef: nout x (P*P) (row o = output o), slot[o] = the
-// workspace block output o writes (out + slot[o]*m*m, ld m).
-template <int P, int VW>
-__global__ void __launch_bounds__(256) premix_kernel(const double* __restrict__ X, int64_t ldx,
-                                                     int64_t m, const double* __restrict__ coef,
-                                                     const int32_t* __restrict__ slot, int nout,
-                                                     double* __restrict__ out) {
-  constexpr int NB = P * P;
-  extern __shared__ double s_coef[];
-  for (int i = threadIdx.x; i < nout * NB; i += blockDim.x) s_coef[i] = coef[i];
-  __syncthreads();
-  const int64_t vpr = m / VW;  // vectors per row
-  const int64_t total = m * vpr;
-  const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / vpr;
-    const int64_t c = (idx - r * vpr) * VW;
-    Vec<VW> x[NB];
+// One term of a combination: acc = acc + c*x.  c = +-1 is a single
+// (negated) add -- bitwise the oracle's separate mul-then-add, since (+-1)*x
+// is exact; other c multiply first (__dmul_rn, never contracted).
+// Accumulators start at -0.0: (-0.0) + v == v for every v (signed zeros
+// included), so the first term needs no special case.
+template <int VW>
+__device__ __forceinline__ void add_term(Vec<VW>& acc, const Vec<VW>& x, int kind, double cf) {
 #pragma unroll
-    for (int k = 0; k < NB; ++k)
-      x[k] = load_vec<VW>(X + ((k / P) * m + r) * ldx + (k % P) * m + c);
-    for (int o = 0; o < nout; ++o) {
-      Vec<VW> acc;
-      bool first = true;
-#pragma unroll
-      for (int k = 0; k < NB; ++k) {
-        const double cf = s_coef[o * NB + k];
-        if (cf != 0.0) {
-#pragma unroll
-          for (int e = 0; e < VW; ++e)
-            acc.v[e] = first ? __dmul_rn(cf, x[k].v[e]) : __dadd_rn(acc.v[e], __dmul_rn(cf, x[k].v[e]));
-          first = false;
-        }
-      }
-      store_vec<VW>(out + (int64_t)slot[o] * mm + r * m + c, acc);
-    }
+  for (int e = 0; e < VW; ++e) {
+    const double v = kind == MIX_GEN ? __dmul_rn(cf, x.v[e]) : (kind == MIX_NEG ? -x.v[e] : x.v[e]);
+    acc.v[e] = __dadd_rn(acc.v[e], v);
   }
 }
 
-// K6: post-addition.  w: (P*P) x RL (row i = C block i); column q is zero
-// for products outside this plan's shard.  active[q] != 0 iff column q has
-// a nonzero.  C_i = alpha * sum_q w[i][q] * P_q (a C block without terms is 0).
-template <int P, int VW>
-__global__ void __launch_bounds__(256) postmix_kernel(const double* __restrict__ Pw, int64_t m,
-                                                      int64_t RL, const double* __restrict__ w,
-                                                      double alpha, double* __restrict__ C,
-                                                      int64_t ldc) {
-  constexpr int NB = P * P;
-  extern __shared__ double s_w[];  // NB x RL, then RL activity flags (as doubles)
-  for (int64_t i = threadIdx.x; i < NB * RL; i += blockDim.x) s_w[i] = w[i];
+// Address of element (r, c) of block/slot `id` in a view: a block view is the
+// P x P partition of a matrix with leading dimension ld (id = br*P + bc); a
+// slot view is a [slots][m][m] workspace.
+struct View {
+  double* base;
+  int64_t ld;
+  int P;         // 0 => slot view
+  __device__ __forceinline__ double* at(int id, int64_t m, int64_t r, int64_t c) const {
+    if (P == 0) return base + (int64_t)id * m * m + r * m + c;
+    return base + ((int64_t)(id / P) * m + r) * ld + (int64_t)(id % P) * m + c;
+  }
+};
+
+// General K4/K6: out_o = alpha * sum_t coef_t * in_{src_t}, for every output
+// row o of the MixRow table, over every position of the m x m blocks.  A CTA
+// owns a segment of 32*VW consecutive positions of one row r; warp w
+// computes outputs w, w+8, ... for that segment along warp-uniform term
+// lists (coalesced 1 KB loads/stores per warp; no data-dependent register
+// indexing, no divergence).  Inputs are loaded with L1 allocation so the
+// re-reads of an input block by the CTA's other outputs hit L1.  Any split
+// factor, any number of terms.
+template <int VW>
+__global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
+                                                  const void* __restrict__ table, int nrow,
+                                                  int nterm, double alpha) {
+  extern __shared__ __align__(16) uint8_t s_raw[];
+  const size_t tbytes = sizeof(MixRow) * nrow + sizeof(MixTerm) * nterm;
+  for (size_t i = threadIdx.x; i < tbytes / 8; i += blockDim.x)
+    reinterpret_cast<uint64_t*>(s_raw)[i] = reinterpret_cast<const uint64_t*>(table)[i];
   __syncthreads();
-  const int64_t vpr = m / VW;
-  const int64_t total = m * vpr;
-  const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / vpr;
-    const int64_t c = (idx - r * vpr) * VW;
-    Vec<VW> acc[NB];
-    bool first[NB];
+  const MixRow* rows = reinterpret_cast<const MixRow*>(s_raw);
+  const MixTerm* terms = reinterpret_cast<const MixTerm*>(rows + nrow);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int SEG = 32 * VW;
+  const int64_t segs_per_row = (m + SEG - 1) / SEG;
+  const int64_t total = m * segs_per_row;
+  for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
+    const int64_t r = seg / segs_per_row;
+    const int64_t c = (seg - r * segs_per_row) * SEG + lane * VW;
+    if (c >= m) continue;
+    for (int o = warp; o < nrow; o += 8) {
+      const MixRow row = rows[o];
+      Vec<VW> acc;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      first[i] = true;
-#pragma unroll
-      for (int e = 0; e < VW; ++e) acc[i].v[e] = 0.0;
-    }
-    for (int64_t q = 0; q < RL; ++q) {
-      bool any = false;
-#pragma unroll
-      for (int i = 0; i < NB; ++i) any |= (s_w[i * RL + q] != 0.0);
-      if (!any) continue;
-      const Vec<VW> x = load_vec<VW>(Pw + q * mm + r * m + c);
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const double cf = s_w[i * RL + q];
-        if (cf != 0.0) {
-#pragma unroll
-          for (int e = 0; e < VW; ++e)
-            acc[i].v[e] = first[i] ? __dmul_rn(cf, x.v[e]) : __dadd_rn(acc[i].v[e], __dmul_rn(cf, x.v[e]));
-          first[i] = false;
-        }
+      for (int e = 0; e < VW; ++e) acc.v[e] = -0.0;
+      int t = row.first;
+      const int tend = row.first + row.count;
+      for (; t + 1 < tend; t += 2) {  // two loads in flight per step
+        const MixTerm t0 = terms[t], t1 = terms[t + 1];
+        const Vec<VW> x0 = load_vec<VW>(in.at(t0.src, m, r, c));
+        const Vec<VW> x1 = load_vec<VW>(in.at(t1.src, m, r, c));
+        add_term<VW>(acc, x0, t0.kind, t0.coef);
+        add_term<VW>(acc, x1, t1.kind, t1.coef);
       }
-    }
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
+      if (t < tend) {
+        const MixTerm t0 = terms[t];
+        add_term<VW>(acc, load_vec<VW>(in.at(t0.src, m, r, c)), t0.kind, t0.coef);
+      }
       if (alpha != 1.0) {
 #pragma unroll
-        for (int e = 0; e < VW; ++e) acc[i].v[e] = __dmul_rn(alpha, acc[i].v[e]);
+        for (int e = 0; e < VW; ++e) acc.v[e] = __dmul_rn(alpha, acc.v[e]);
       }
-      store_vec<VW>(C + ((i / P) * m + r) * ldc + (i % P) * m + c, acc[i]);
+      store_vec<VW>(out.at(row.target, m, r, c), acc);
     }
   }
-}
-
-int grid_for(int64_t work) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t blocks = (work + 255) / 256;
-  int64_t cap = (int64_t)sms * 8;  // 8 x 256 threads resident per SM
-  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
 }
 
 bool aligned(const void* p, int bytes) { return ((uintptr_t)p % bytes) == 0; }
 
-template <int P, int VW>
-cudaError_t premix_launch(const MixTable& t, const double* X, int64_t ldx, int64_t m, double* out,
-                          const int32_t* d_slot, cudaStream_t s) {
-  constexpr int NB = P * P;
-  size_t smem = sizeof(double) * (size_t)t.nout * NB;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(premix_kernel<P, VW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  premix_kernel<P, VW><<<grid_for(m * (m / VW)), 256, smem, s>>>(X, ldx, m, t.d_coef, d_slot,
-                                                                  t.nout, out);
-  return cudaGetLastError();
+// Grid: `work` items of `per_block` each, capped at 8 CTAs (of 256 threads) per SM.
+int grid_for(int64_t work, int per_block) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (work + per_block - 1) / per_block;
+  const int64_t cap = (int64_t)sms * 8;
+  return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
 }
 
-template <int P, int VW>
-cudaError_t postmix_launch(const Plan& pl, double alpha, const double* Pw, double* C, int64_t ldc,
-                           cudaStream_t s) {
-  constexpr int NB = P * P;
-  size_t smem = sizeof(double) * (size_t)NB * pl.RL;
+template <int VW>
+cudaError_t mix_launch(const MixTable& t, View in, View out, int64_t m, double alpha, cudaStream_t s) {
+  const size_t smem = sizeof(MixRow) * t.nrow + sizeof(MixTerm) * t.nterm;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(postmix_kernel<P, VW>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(mix_kernel<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
   }
-  postmix_kernel<P, VW><<<grid_for(pl.m * (pl.m / VW)), 256, smem, s>>>(
-      Pw, pl.m, pl.RL, pl.mixC.d_coef, alpha, C, ldc);
+  mix_kernel<VW><<<grid_for(m * ((m + 32 * VW - 1) / (32 * VW)), 1), 256, smem, s>>>(
+      in, out, m, t.d_table, t.nrow, t.nterm, alpha);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 // Vector width: 256-bit when every row start is 32-byte aligned, else 128/64-bit.
-static int pick_vw(int P, int64_t m, std::initializer_list<std::pair<const void*, int64_t>> views) {
-  int max_vw = P <= 4 ? 4 : (P <= 6 ? 2 : 1);
+static int pick_vw(int64_t m, std::initializer_list<std::pair<const void*, int64_t>> views) {
+  int max_vw = 4;
+  if (const char* e = getenv("MF_MIX_VW")) {  // tuning knob for experiments: 1, 2 or 4
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4) max_vw = v;
+  }
   for (int vw = max_vw; vw > 1; vw /= 2) {
     bool ok = (m % vw) == 0;
     for (auto& v : views) ok = ok && aligned(v.first, 8 * vw) && (v.second % vw) == 0;
@@ -196,43 +191,31 @@ static int pick_vw(int P, int64_t m, std::initializer_list<std::pair<const void*
   return 1;
 }
 
-#define MF_DISPATCH_P(P_, VW_, CALL)                                   \
-  switch (P_) {                                                        \
-    case 1: CALL(1, VW_); break;                                       \
-    case 2: CALL(2, VW_); break;                                       \
-    case 3: CALL(3, VW_); break;                                       \
-    case 4: CALL(4, VW_); break;                                       \
-    default: return cudaErrorInvalidValue;                             \
-  }
+static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, int64_t m,
+                                double alpha, cudaStream_t s) {
+  if (t.nrow == 0) return cudaSuccess;
+  if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s);
+  if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s);
+  return mix_launch<1>(t, in, out, m, alpha, s);
+}
 
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s) {
-  if (t.nout == 0) return cudaSuccess;
-  const int32_t* d_slot = reinterpret_cast<const int32_t*>(t.d_coef + (size_t)t.nout * t.nin);
-  int vw = pick_vw(pl.P, pl.m, {{X, ldx}, {out, pl.m}});
-#define PRE(P_, VW_) return premix_launch<P_, VW_>(t, X, ldx, pl.m, out, d_slot, s)
-  if (pl.P == 6) { if (vw >= 2) PRE(6, 2); PRE(6, 1); }
-  if (pl.P == 8) PRE(8, 1);
-  if (pl.P == 9) PRE(9, 1);
-  if (vw == 4) { MF_DISPATCH_P(pl.P, 4, PRE); }
-  else if (vw == 2) { MF_DISPATCH_P(pl.P, 2, PRE); }
-  else { MF_DISPATCH_P(pl.P, 1, PRE); }
-#undef PRE
-  return cudaErrorInvalidValue;
+  if (t.nrow == 0) return cudaSuccess;
+  if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
+    return launch_premix_fixed(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s);
+  const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
+  return mix_dispatch(vw, t, View{const_cast<double*>(X), ldx, pl.P}, View{out, pl.m, 0}, pl.m,
+                      1.0, s);
 }
 
 cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C, int64_t ldc,
                            cudaStream_t s) {
-  int vw = pick_vw(pl.P, pl.m, {{Pw, pl.m}, {C, ldc}});
-#define POST(P_, VW_) return postmix_launch<P_, VW_>(pl, alpha, Pw, C, ldc, s)
-  if (pl.P == 6) { if (vw >= 2) POST(6, 2); POST(6, 1); }
-  if (pl.P == 8) POST(8, 1);
-  if (pl.P == 9) POST(9, 1);
-  if (vw == 4) { MF_DISPATCH_P(pl.P, 4, POST); }
-  else if (vw == 2) { MF_DISPATCH_P(pl.P, 2, POST); }
-  else { MF_DISPATCH_P(pl.P, 1, POST); }
-#undef POST
-  return cudaErrorInvalidValue;
+  if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
+    return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s);
+  const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
+  return mix_dispatch(vw, pl.mixC, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
+                      pl.m, alpha, s);
 }
 
 }  // namespace mf

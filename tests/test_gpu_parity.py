@@ -96,10 +96,23 @@ def _flat_oracle_triple(name, levels):
     return oracle.kron_power(oracle.catalog(name), levels)
 
 
+MIX_PATHS = ["fixed", "generic"]  # compile-time specialised K4/K6 vs table-driven kernels
+
+
+def _mix_path(monkeypatch, path):
+    if path == "generic":
+        monkeypatch.setenv("MF_MIX_GENERIC", "1")
+    else:
+        monkeypatch.delenv("MF_MIX_GENERIC", raising=False)
+
+
+@pytest.mark.parametrize("path", MIX_PATHS)
 @pytest.mark.parametrize("name,levels,n", [(SW, 1, 64), (SW, 1, 200), ("laderman", 1, 96),
                                            (SW, 2, 256), ("paper-strassen", 1, 128),
-                                           ("strassen-1969", 1, 64)])
-def test_premix_bit_exact(name, levels, n):
+                                           ("strassen-1969", 1, 64), ("paper-strassen", 2, 128),
+                                           ("strassen-1969", 2, 64), (SW, 3, 128)])
+def test_premix_bit_exact(name, levels, n, path, monkeypatch):
+    _mix_path(monkeypatch, path)
     A, B = mf_inputs.pair("uniform", n, 5)
     to = _flat_oracle_triple(name, levels)
     with mf.Plan(triples.get(name), levels, n) as p:
@@ -117,9 +130,12 @@ def test_premix_bit_exact(name, levels, n):
                 assert (got[idx[q]] == ref[q]).all(), (side, q)
 
 
+@pytest.mark.parametrize("path", MIX_PATHS)
 @pytest.mark.parametrize("name,levels,n", [(SW, 1, 64), ("laderman", 1, 96), (SW, 2, 256),
-                                           (SW, 1, 200)])
-def test_postmix_bit_exact(name, levels, n):
+                                           (SW, 1, 200), ("paper-strassen", 2, 128),
+                                           ("strassen-1969", 1, 64), (SW, 3, 128)])
+def test_postmix_bit_exact(name, levels, n, path, monkeypatch):
+    _mix_path(monkeypatch, path)
     to = _flat_oracle_triple(name, levels)
     m = n // to.p
     rng = np.random.Generator(np.random.PCG64(9))
@@ -156,13 +172,15 @@ def test_leaf_stage_matches_oracle_products_on_integers():
 
 CASES = [(SW, 1, 64), (SW, 1, 256), (SW, 1, 400), (SW, 2, 128), (SW, 2, 512), (SW, 3, 512),
          ("paper-strassen", 1, 256), ("paper-strassen", 2, 256), ("strassen-1969", 1, 256),
-         ("laderman", 1, 96), ("laderman", 1, 288), ("laderman", 1, 390),
+         ("laderman", 1, 96), ("laderman", 1, 288), ("laderman", 1, 390), ("laderman", 2, 144),
          ("classical-p2", 1, 128)]
 
 
+@pytest.mark.parametrize("path", MIX_PATHS)
 @pytest.mark.parametrize("name,levels,n", CASES)
-def test_dgemm_integer_exact(name, levels, n):
+def test_dgemm_integer_exact(name, levels, n, path, monkeypatch):
     """integer computations are exact -> bit-exact vs the exact product."""
+    _mix_path(monkeypatch, path)
     A, B = mf_inputs.pair("int1024", n, 11)
     C = run(name, levels, A, B)
     assert (C == exact(A, B)).all()
