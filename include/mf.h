@@ -69,6 +69,10 @@ typedef struct {
                            (C summed onto every rank)                             */
   int32_t profile;      /* 1: mf_dgemm records CUDA events around each phase on
                            the call's stream (read with mf_profile_read)          */
+  int32_t host_only;    /* 1: plan the host logic only (Brent check, flattening,
+                           classification, sharding) -- no device, no workspace;
+                           mf_plan_info / mf_plan_products work, compute calls
+                           return MF_ERR_INVALID_ARG                              */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.

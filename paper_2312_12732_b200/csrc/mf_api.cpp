@@ -217,7 +217,7 @@ mf_status upload_table(MixTable& t) {
 }
 
 void free_plan(Plan* pl) {
-  if (!pl) return;
+  if (!pl || pl->opt.host_only) return;
   DeviceGuard g(pl->device);
   cudaDeviceSynchronize();
   for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_table,
@@ -312,11 +312,13 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     return fail(MF_ERR_INVALID_ARG, "shard_count %d exceeds the %lld leaf products", shard_count,
                 (long long)RL);
 
-  DeviceGuard guard(o.device);
+  const bool host_only = o.host_only != 0;
+  DeviceGuard guard(host_only ? -1 : o.device);
   if (!guard.ok) return fail(MF_ERR_CUDA, "cannot select device %d", o.device);
   std::unique_ptr<mf_plan_st> pl(new (std::nothrow) mf_plan_st());
   if (!pl) return fail(MF_ERR_OUT_OF_MEMORY, "host allocation");
-  MF_CUDA(cudaGetDevice(&pl->device), "cudaGetDevice");
+  if (!host_only) MF_CUDA(cudaGetDevice(&pl->device), "cudaGetDevice");
+  else pl->device = -1;
   pl->p = p; pl->R = R; pl->levels = levels; pl->n = n;
   pl->P = (int)P; pl->RL = RL; pl->m = n / P;
   pl->opt = o; pl->leaf = o.leaf;
@@ -394,6 +396,12 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     for (int i = 0; i < NB; ++i) c.out_map.push_back(i);
     for (int32_t q : pl->my_prods)
       for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+  }
+
+  if (host_only) {  // host logic only: no device work, no workspace
+    pl->n_jobs = (int)pl->my_prods.size();
+    *out = pl.release();
+    return MF_OK;
   }
 
   // ---- device allocations ----
@@ -483,6 +491,7 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
                    int64_t ldb, double* C, int64_t ldc, void* stream) {
   g_err.clear();
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   const int64_t n = pl->n;
   const bool root_inputs = pl->nccl_comm && pl->opt.input_mode == MF_IN_ROOT;
   const bool is_root = pl->shard_rank == 0;
@@ -580,6 +589,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
                         int64_t ldb, double* C, int64_t ldc, void* stream) {
   g_err.clear();
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   const int64_t n = pl->n;
   mf_status st;
   if ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK ||
@@ -607,6 +617,7 @@ mf_status mf_premix(mf_plan_t pl, int32_t side, const double* X, int64_t ldx, do
                     void* stream) {
   g_err.clear();
   if (!pl || !X || !out || (side != 0 && side != 1)) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no pre-additions");
   DeviceGuard guard(pl->device);
   MF_CUDA(launch_premix(*pl, side == 0 ? pl->mixA : pl->mixB, X, ldx, out,
@@ -619,6 +630,7 @@ mf_status mf_leaf(mf_plan_t pl, const double* A, int64_t lda, const double* B, i
                   const double* T, const double* S, double* P, void* stream) {
   g_err.clear();
   if (!pl || !A || !B || !P) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   DeviceGuard guard(pl->device);
   return run_leaf(*pl, A, lda, B, ldb, T, S, P, pl->m, pl->m * pl->m, 1.0,
                   static_cast<cudaStream_t>(stream));
@@ -628,6 +640,7 @@ mf_status mf_postmix(mf_plan_t pl, double alpha, const double* P, double* C, int
                      void* stream) {
   g_err.clear();
   if (!pl || !P || !C) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no post-addition");
   DeviceGuard guard(pl->device);
   MF_CUDA(launch_postmix(*pl, alpha, P, C, ldc, static_cast<cudaStream_t>(stream)), "post-add (K6)");

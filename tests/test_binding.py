@@ -107,3 +107,30 @@ def test_plan_accepts_dyadic_rescaling_up_to_device():
     t = triples.STRASSEN_WINOGRAD
     st, msg = _plan_status(2, 7, t.U / 2, t.V, t.W * 2, 1, 64)
     assert st in (mf.MF_OK, mf.MF_ERR_CUDA, mf.MF_ERR_OUT_OF_MEMORY), msg
+
+
+@pytest.mark.parametrize("name,levels,nmat", [("strassen-winograd", 1, 4), ("strassen-winograd", 2, 40),
+                                              ("laderman", 1, 14), ("paper-strassen", 1, 4)])
+def test_host_only_plan_classification(name, levels, nmat):
+    """mf_plan step 5 on the host: single +-1 columns alias (SURVEY App. A:
+    SW 4 T + 4 S materialised, SW^2 40 + 40, Laderman 14 + 14)."""
+    t = triples.get(name)
+    p = mf.Plan(t, levels, t.p ** levels * 8, host_only=True)
+    info = p.info()
+    assert info["n_products"] == t.R ** levels and info["workspace_bytes"] == 0
+    assert info["n_mat_a"] == nmat and info["n_mat_b"] == nmat
+    pr = p.products()
+    assert (pr["a_src"] == 1).sum() == nmat and (pr["shard"] == 0).all()
+    # aliased operands carry their block index, materialised ones a dense slot index
+    assert sorted(pr["a_idx"][pr["a_src"] == 1].tolist()) == list(range(nmat))
+    with pytest.raises(mf.MfError):
+        import torch
+        p.dgemm(torch.zeros(1), torch.zeros(1))
+
+
+def test_host_only_sharding_balanced():
+    p = mf.Plan(triples.STRASSEN_WINOGRAD, 2, 64, shard_rank=0, shard_count=8, host_only=True)
+    sh = p.products()["shard"]
+    counts = np.bincount(sh, minlength=8)
+    assert counts.sum() == 49 and counts.max() - counts.min() <= 1
+    assert (np.diff(sh) >= 0).all()  # contiguous ranges

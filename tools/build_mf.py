@@ -67,6 +67,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [nvcc(), *ARCH, "-lineinfo", *common, "-c", path, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
+            # Tag::T is used only as a template argument (constant expression);
+            # nvcc's "host member read in device function" diagnostic is spurious there.
+            cmd += ["-diag-suppress", "20094"]
         else:
             cmd += ["-x", "cu"]  # host-only TU compiled by nvcc for the CUDA headers
         if verbose:
