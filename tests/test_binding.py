@@ -123,9 +123,9 @@ def test_host_only_plan_classification(name, levels, nmat):
     assert (pr["a_src"] == 1).sum() == nmat and (pr["shard"] == 0).all()
     # aliased operands carry their block index, materialised ones a dense slot index
     assert sorted(pr["a_idx"][pr["a_src"] == 1].tolist()) == list(range(nmat))
-    with pytest.raises(mf.MfError):
-        import torch
-        p.dgemm(torch.zeros(1), torch.zeros(1))
+    buf = np.zeros(16)
+    st = mf._lib.mf_dgemm(p._h, 1.0, buf.ctypes.data, 4, buf.ctypes.data, 4, buf.ctypes.data, 4, None)
+    assert st == mf.MF_ERR_INVALID_ARG and "host-only" in mf._lib.mf_last_error().decode()
 
 
 def test_host_only_sharding_balanced():
