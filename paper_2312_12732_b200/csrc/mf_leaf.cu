@@ -237,6 +237,36 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
   nj_stride = prm.bmode == B_ROWS ? 16 * 8 : 2048;
 
+  // Fragment double buffering: group g+1's LDS are issued before group g's 64
+  // DMMAs, so no k-group starts on an LDS-latency bubble.  A stage's slot is
+  // released (mbarrier.arrive has release semantics: the LDS reads are
+  // complete) as soon as its last fragment load has been issued.
+  double fa0[8][2], fb0[2][2][2], fa1[8][2], fb1[2][2][2];
+  auto load_frags = [&](uint32_t sA, uint32_t sB, int g, double (&fa)[8][2], double (&fb)[2][2][2]) {
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, fa[mi][0], fa[mi][1]);
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+        lds128(sB + offB[g][s2] + nj * nj_stride, fb[nj][s2][0], fb[nj][s2][1]);
+  };
+  auto mma_group = [&](const double (&fa)[8][2], const double (&fb)[2][2][2]) {
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            dmma(acc[mi][nj][j][0], acc[mi][nj][j][1], fa[mi][s2], fb[nj][s2][j]);
+  };
+
+  if (prm.kblocks > 0) {
+    mbar_wait(full0, 0);
+    load_frags(s_base, s_base + A_BYTES, 0, fa0, fb0);
+  }
   for (int kb = 0; kb < prm.kblocks; ++kb) {
     if (warp == 0) {
       const int kn = kb + STAGES - 1;  // refill the slot consumed at kb - 1
@@ -246,31 +276,18 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
     }
     const int s = kb % STAGES;
-    mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
     const uint32_t sA = s_base + s * STAGE_BYTES, sB = sA + A_BYTES;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      double a[8][2];  // [mi][s]
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, a[mi][0], a[mi][1]);
-      double b[2][2][2];  // [nj][s][j]
-#pragma unroll
-      for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2)
-          lds128(sB + offB[g][s2] + nj * nj_stride, b[nj][s2][0], b[nj][s2][1]);
-#pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2)
-#pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-              dmma(acc[mi][nj][j][0], acc[mi][nj][j][1], a[mi][s2], b[nj][s2][j]);
-    }
+    load_frags(sA, sB, 1, fa1, fb1);  // group 1 of this stage
+    mma_group(fa0, fb0);              // group 0 of this stage
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    if (kb + 1 < prm.kblocks) {       // group 0 of the next stage
+      const int s1 = (kb + 1) % STAGES;
+      mbar_wait(full0 + 8 * s1, ((kb + 1) / STAGES) & 1);
+      const uint32_t nA = s_base + s1 * STAGE_BYTES;
+      load_frags(nA, nA + A_BYTES, 0, fa0, fb0);
+    }
+    mma_group(fa1, fb1);              // group 1 of this stage
   }
 
   // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
