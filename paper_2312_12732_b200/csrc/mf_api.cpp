@@ -227,6 +227,9 @@ void free_plan(Plan* pl) {
   if (pl->done) cudaEventDestroy(pl->done);
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
+  for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
+  if (pl->h2d) cudaStreamDestroy(pl->h2d);
+  if (pl->d2h) cudaStreamDestroy(pl->d2h);
 }
 
 // Events of the current call when profiling is on (nullptr otherwise).
@@ -249,13 +252,14 @@ bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_
 
 mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
                    const double* T, const double* S, double* out, int64_t ldo, int64_t stride,
-                   double alpha, cudaStream_t s) {
+                   double alpha, cudaStream_t s, Rows rows = Rows()) {
   LeafArgs a;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
   a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
   a.P = pl.P; a.m = pl.m;
   a.out = out; a.ldo = ldo; a.out_block_stride = stride; a.alpha = alpha;
   a.jobs = pl.d_jobs; a.n_jobs = pl.n_jobs;
+  a.rows = rows;
   MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
   return MF_OK;
 }
@@ -585,6 +589,18 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
   return MF_OK;
 }
 
+// Host-buffer pipeline: B is copied first and pre-added, then
+// the path runs slab by slab over row ranges [r*h, (r+1)*h) of every block:
+// H2D of A's slab r (copy stream) -> K4(A) / K5 / K6 on those rows (the call's
+// stream) -> D2H of C's slab r (second copy stream), so the PCIe transfers of
+// slab r+1 and r-1 overlap the compute of slab r.
+static int pipeline_slabs(const Plan& pl) {
+  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA) return 1;
+  for (int ns : {8, 4, 2})
+    if (pl.m % ((int64_t)ns * 128) == 0) return ns;
+  return 1;
+}
+
 mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* C, int64_t ldc, void* stream) {
   g_err.clear();
@@ -601,15 +617,74 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   if (!pl->hA && cudaMalloc(&pl->hA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device A");
   if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B");
   if (!pl->hC && cudaMalloc(&pl->hC, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C");
-  MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
-  MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
-  mf_options saved = pl->opt;
-  pl->opt.input_mode = MF_IN_REPLICATED;
-  st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
-  pl->opt = saved;
-  if (st != MF_OK) return st;
-  MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
-  MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+  const int ns = pipeline_slabs(*pl);
+  if (ns == 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
+    MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+    MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
+    mf_options saved = pl->opt;
+    pl->opt.input_mode = MF_IN_REPLICATED;
+    st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
+    pl->opt = saved;
+    if (st != MF_OK) return st;
+    MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+    MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    return MF_OK;
+  }
+  if (!pl->h2d) MF_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking), "stream");
+  if (!pl->d2h) MF_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking), "stream");
+  const size_t nev = 3 + 2 * ns;  // start, B ready, done, A slab r ready, C slab r ready
+  while (pl->pipe_events.size() < nev) {
+    cudaEvent_t e;
+    MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    pl->pipe_events.push_back(e);
+  }
+  cudaEvent_t e_start = pl->pipe_events[0], e_b = pl->pipe_events[1], e_done = pl->pipe_events[2];
+  cudaEvent_t* e_a = &pl->pipe_events[3];
+  cudaEvent_t* e_c = &pl->pipe_events[3 + ns];
+  const int64_t m = pl->m, h = m / ns;
+  const int P = pl->P;
+  // prior work on the call's stream (which may still read the plan buffers) first
+  MF_CUDA(cudaEventRecord(e_start, s), "event");
+  MF_CUDA(cudaStreamWaitEvent(pl->h2d, e_start, 0), "wait");
+  MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_start, 0), "wait");
+  MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, pl->h2d), "H2D B");
+  MF_CUDA(cudaEventRecord(e_b, pl->h2d), "event");
+  for (int r = 0; r < ns; ++r) {
+    for (int br = 0; br < P; ++br) {
+      const int64_t row = br * m + r * h;
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8, h,
+                                cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
+    }
+    MF_CUDA(cudaEventRecord(e_a[r], pl->h2d), "event");
+  }
+  const double* dA = pl->hA;
+  const double* dB = pl->hB;
+  double* dC = pl->hC;
+  MF_CUDA(cudaStreamWaitEvent(s, e_b, 0), "wait");
+  if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, s), "pre-add B (K4)");
+  for (int r = 0; r < ns; ++r) {
+    const Rows rows{r * h, (r + 1) * h};
+    MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
+    if (pl->levels == 0) {
+      if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, s, rows)) != MF_OK)
+        return st;
+    } else {
+      MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
+      if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, rows)) != MF_OK)
+        return st;
+      MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, dC, n, s, rows), "post-add (K6)");
+    }
+    MF_CUDA(cudaEventRecord(e_c[r], s), "event");
+    MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_c[r], 0), "wait");
+    for (int br = 0; br < P; ++br) {
+      const int64_t row = br * m + r * h;
+      MF_CUDA(cudaMemcpy2DAsync(C + row * ldc, ldc * 8, dC + row * n, n * 8, n * 8, h,
+                                cudaMemcpyDeviceToHost, pl->d2h), "D2H C slab");
+    }
+  }
+  MF_CUDA(cudaEventRecord(e_done, pl->d2h), "event");
+  MF_CUDA(cudaStreamWaitEvent(s, e_done, 0), "wait");  // keep the call's stream ordered after D2H
+  MF_CUDA(cudaEventSynchronize(e_done), "cudaEventSynchronize");
   return MF_OK;
 }
 

@@ -91,16 +91,26 @@ struct Plan {
   // NCCL
   void* nccl_comm = nullptr;
   cudaEvent_t done = nullptr;
+  // host-buffer pipeline (mf_dgemm_host): copy streams and per-slab events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> pipe_events;
   // phase profiling (mf_options.profile): 6 events per mf_dgemm call
   std::vector<std::vector<cudaEvent_t>> prof_events;
   size_t prof_used = 0;
 };
 
+// Rows [r0, r1) of every m x m block a launch covers (the whole block by
+// default); the host-buffer pipeline runs the path slab by slab.
+struct Rows {
+  int64_t r0 = 0, r1 = -1;  // r1 < 0 => m
+  int64_t end(int64_t m) const { return r1 < 0 ? m : r1; }
+};
+
 // ---- launchers (mf_mix.cu, mf_leaf.cu); return cudaError_t of the launch ----
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
-                          double* out, cudaStream_t s);
+                          double* out, cudaStream_t s, Rows rows = Rows());
 cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C,
-                           int64_t ldc, cudaStream_t s);
+                           int64_t ldc, cudaStream_t s, Rows rows = Rows());
 
 struct LeafArgs {
   // operand views: matrices (4-D block view, SRC_INPUT) and workspaces (3-D)
@@ -115,6 +125,7 @@ struct LeafArgs {
   int64_t out_block_stride;  // elements between consecutive output blocks (0 => single)
   double alpha;
   const LeafJob* jobs; int n_jobs;
+  Rows rows;      // output rows of each product computed (r0 multiple of 128)
 };
 bool leaf_tma_supported(const LeafArgs& a);
 
@@ -122,9 +133,9 @@ bool leaf_tma_supported(const LeafArgs& a);
 int fixed_match(const Plan& pl);
 bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t ldb);
 cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
-                                double* out, cudaStream_t s);
+                                double* out, cudaStream_t s, Rows rows);
 cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
-                                 int64_t ldc, cudaStream_t s);
+                                 int64_t ldc, cudaStream_t s, Rows rows);
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s);
 
 }  // namespace mf

@@ -62,6 +62,7 @@ enum BMode : int { B_ROWS = 0, B_BOXES = 1, B_5D = 2 };
 
 struct LeafParams {
   int64_t m;
+  int tm0;  // first tile row (row slab of the host-buffer pipeline)
   int tiles_m, tiles_n, kblocks;
   int bmode;
   double* out;
@@ -154,7 +155,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int group_tiles = GROUP_M * prm.tiles_n;
   const int first_m = (t / group_tiles) * GROUP_M;
   const int gsz = min(prm.tiles_m - first_m, GROUP_M);
-  const int tm = first_m + (t % group_tiles) % gsz;
+  const int tm = prm.tm0 + first_m + (t % group_tiles) % gsz;
   const int tn = (t % group_tiles) / gsz;
   const LeafJob job = prm.jobs[job_id];
 
@@ -326,7 +327,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 // describe (odd m or odd leading dimension).
 struct SimpleParams {
   const double *A, *B, *T, *S;
-  int64_t lda, ldb, m;
+  int64_t lda, ldb, m, r0, r1;
   double* out;
   int64_t ldo, out_stride;
   double alpha;
@@ -335,9 +336,9 @@ struct SimpleParams {
 
 __global__ void leaf_simple_kernel(const SimpleParams prm) {
   const LeafJob job = prm.jobs[blockIdx.z];
-  const int64_t r = (int64_t)blockIdx.y * 16 + threadIdx.y;
+  const int64_t r = prm.r0 + (int64_t)blockIdx.y * 16 + threadIdx.y;
   const int64_t c = (int64_t)blockIdx.x * 16 + threadIdx.x;
-  if (r >= prm.m || c >= prm.m) return;
+  if (r >= prm.r1 || c >= prm.m) return;
   const int64_t mm = prm.m * prm.m;
   const double* X;
   int64_t ldx;
@@ -438,8 +439,9 @@ bool leaf_tma_supported(const LeafArgs& a) {
 }
 
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
-  if (a.n_jobs == 0 || a.m == 0) return cudaSuccess;
-  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a)) {
+  const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m);
+  if (a.n_jobs == 0 || a.m == 0 || r1 <= r0) return cudaSuccess;
+  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && r0 % BM == 0) {
     int bmode = B_ROWS;  // measured fastest (profiles/leaf_bmode_r01.json)
     if (const char* e = getenv("MF_LEAF_BMODE")) bmode = atoi(e);  // experiments: 0, 1, 2
     if (bmode == B_5D && a.m % 16 != 0) bmode = B_BOXES;
@@ -475,7 +477,8 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     }
     LeafParams prm;
     prm.m = a.m;
-    prm.tiles_m = (int)((a.m + BM - 1) / BM);
+    prm.tm0 = (int)(r0 / BM);
+    prm.tiles_m = (int)((r1 - r0 + BM - 1) / BM);
     prm.tiles_n = (int)((a.m + BN - 1) / BN);
     prm.kblocks = (int)((a.m + BK - 1) / BK);
     prm.bmode = bmode;
@@ -489,9 +492,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     leaf_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mT, mB, mS, prm);
     return cudaGetLastError();
   }
-  SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, a.out, a.ldo, a.out_block_stride,
-                   a.alpha, a.jobs};
-  dim3 grid((unsigned)((a.m + 15) / 16), (unsigned)((a.m + 15) / 16), (unsigned)a.n_jobs);
+  SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, a.out, a.ldo,
+                   a.out_block_stride, a.alpha, a.jobs};
+  dim3 grid((unsigned)((a.m + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), (unsigned)a.n_jobs);
   leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
   return cudaGetLastError();
 }

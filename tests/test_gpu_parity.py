@@ -37,7 +37,12 @@ def host(X):
 
 
 def exact(A, B):
-    return (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    """Exact product of integer-valued inputs: numpy int64 matmul for small n,
+    the oracle's classical loop beyond (exact while |partial sums| < 2^53)."""
+    if A.shape[0] <= 512:
+        return (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    assert np.abs(A).max() * np.abs(B).max() * A.shape[0] < 2.0 ** 53
+    return oracle.classical(A, B)
 
 
 def run(name, levels, A, B, alpha=1.0, leaf="dmma"):
@@ -258,6 +263,27 @@ def test_host_buffer_entry_point():
         assert (C == exact(A, B)).all()
         C2 = p.dgemm_host(A, B, alpha=2.0)
         assert (C2 == 2 * exact(A, B)).all()
+
+
+@pytest.mark.parametrize("path", MIX_PATHS)
+@pytest.mark.parametrize("name,levels,n", [(SW, 2, 2048), (SW, 1, 2048), (None, 0, 1024),
+                                           ("laderman", 1, 3072), (SW, 1, 1000)])
+def test_host_pipeline_matches_device_path(name, levels, n, path, monkeypatch):
+    """mf_dgemm_host's slab pipeline (H2D / K4-K5-K6 per row slab / D2H on
+    three streams) computes exactly what mf_dgemm computes: same kernels, same
+    per-element order -> bitwise equal on random inputs, exact on integers;
+    host leading dimensions > n are honoured."""
+    _mix_path(monkeypatch, path)
+    t = triples.get(name) if name else None
+    A, B = mf_inputs.pair("uniform", n, 15)
+    with mf.Plan(t, levels, n) as p:
+        Cd = host(p.dgemm(dev(A), dev(B), alpha=0.75))
+        Ah = np.zeros((n, n + 8)); Ah[:, :n] = A
+        Ch = np.full((n, n + 4), np.nan)
+        p.dgemm_host_ptr(Ah.ctypes.data, n + 8, B.ctypes.data, n, Ch.ctypes.data, n + 4, alpha=0.75)
+        assert (Ch[:, :n] == Cd).all() and np.isnan(Ch[:, n:]).all()
+        Ai, Bi = mf_inputs.pair("int1024", n, 16)
+        assert (p.dgemm_host(Ai, Bi) == exact(Ai, Bi)).all()
 
 
 def test_invalid_calls_report_errors():
