@@ -35,8 +35,29 @@ UNIT = "TFLOPS"
 CPU_SAMPLE_N = 4096  # oracle sample: same triple and levels at n/4 (1/64 of the work)
 
 
+def cpu_sample_n(a):
+    """n of the bounded oracle sample: n/4 capped at 4096, divisible by p^levels."""
+    p = {"laderman": 3, "classical-p3": 3}.get(a.triple, 2) ** a.levels
+    ns = min(max(a.n // 4, p), CPU_SAMPLE_N)
+    return max(p, ns - ns % p)
+
+
+# BASELINE.json configs as presets: (n, triple, levels)
+CONFIGS = {
+    "c1-sw1-64": (64, "strassen-winograd", 1),
+    "c2-sw1-4096": (4096, "strassen-winograd", 1),
+    "c3-sw2-16384": (16384, "strassen-winograd", 2),      # the metric's config (default)
+    "c3b-sw1-16384": (16384, "strassen-winograd", 1),
+    "c4a-ld1-13824": (13824, "laderman", 1),
+    "c4b-sw2-13824": (13824, "strassen-winograd", 2),     # <4,4,4;49> = SW (x) SW
+    "c5-sw2-32768": (32768, "strassen-winograd", 2),      # config 5's problem (1-GPU leg)
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=None,
+                    help="BASELINE config preset (overrides --n/--triple/--levels)")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -47,7 +68,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-classical", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config:
+        a.n, a.triple, a.levels = CONFIGS[a.config]
+    return a
 
 
 def workload_name(a):
@@ -60,9 +84,12 @@ def _rank(a):
 
 
 def config(a, world):
-    return {"workload": workload_name(a), "n": a.n, "triple": a.triple, "levels": a.levels,
+    return {"workload": workload_name(a), "preset": a.config, "n": a.n, "triple": a.triple,
+            "levels": a.levels,
             "leaf_products": _rank(a) ** a.levels, "inputs": "uniform[-1,1) fp64, seeds 0/1",
-            "l2": "inputs larger than L2 (8n^2 = %.1f GB per matrix); no flush" % (8 * a.n ** 2 / 1e9),
+            "l2": ("inputs larger than L2 (8n^2 = %.1f GB per matrix); no flush" % (8 * a.n ** 2 / 1e9)
+                   if 8 * a.n ** 2 > 126e6 else "inputs fit in L2 (%.1f MB per matrix); not flushed"
+                   % (8 * a.n ** 2 / 1e6)),
             "parallelism": f"product-sharded x{world}" if world > 1 else "single GPU"}
 
 
@@ -136,7 +163,7 @@ def cpu_baseline(a):
     import numpy as np
     import mf_inputs
     import oracle
-    n = CPU_SAMPLE_N
+    n = cpu_sample_n(a)
     A, B = mf_inputs.pair("uniform", n, 0)
     t = oracle.catalog(a.triple)
     t0 = time.perf_counter()
@@ -145,7 +172,7 @@ def cpu_baseline(a):
     return {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "cores": oracle.num_threads(),
             "kind": "oracle",
             "sample": f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} "
-                      f"(1/{(a.n // n) ** 3} of the n={a.n} work), {dt:.2f} s; value = 2n^3/t at n={n}",
+                      f"({(n / a.n) ** 3:.4g} of the n={a.n} work), {dt:.2f} s; value = 2n^3/t at n={n}",
             "seconds": dt}
 
 
@@ -156,7 +183,7 @@ def run_reference(a):
         return
     import mf_inputs
     import oracle
-    n = CPU_SAMPLE_N
+    n = cpu_sample_n(a)
     A, B = mf_inputs.pair("uniform", n, 0)
     t = oracle.catalog(a.triple)
     for _ in range(a.warmup):
@@ -169,7 +196,7 @@ def run_reference(a):
     dt = sum(times) / len(times)
     value = 2.0 * n ** 3 / dt / 1e12
     sample = (f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} per step "
-              f"(1/{(a.n // n) ** 3} of the n={a.n} work); value = 2n^3/t at n={n}")
+              f"({(n / a.n) ** 3:.4g} of the n={a.n} work); value = 2n^3/t at n={n}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,

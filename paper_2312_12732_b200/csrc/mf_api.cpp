@@ -594,11 +594,20 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 // H2D of A's slab r (copy stream) -> K4(A) / K5 / K6 on those rows (the call's
 // stream) -> D2H of C's slab r (second copy stream), so the PCIe transfers of
 // slab r+1 and r-1 overlap the compute of slab r.
+// Slab r covers tile rows [r*tm/ns, (r+1)*tm/ns) of 128 rows (the last slab
+// ends at m), so any m with >= 2 tile rows pipelines.
 static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA) return 1;
-  for (int ns : {8, 4, 2})
-    if (pl.m % ((int64_t)ns * 128) == 0) return ns;
-  return 1;
+  const int64_t tiles = (pl.m + 127) / 128;
+  return (int)std::min<int64_t>(8, tiles);
+}
+
+static Rows slab_rows(const Plan& pl, int r, int ns) {
+  const int64_t tiles = (pl.m + 127) / 128;
+  Rows rows;
+  rows.r0 = std::min<int64_t>(pl.m, 128 * (r * tiles / ns));
+  rows.r1 = std::min<int64_t>(pl.m, 128 * ((r + 1) * tiles / ns));
+  return rows;
 }
 
 mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
@@ -618,7 +627,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B");
   if (!pl->hC && cudaMalloc(&pl->hC, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C");
   const int ns = pipeline_slabs(*pl);
-  if (ns == 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
+  if (ns <= 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
     MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
     MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
     mf_options saved = pl->opt;
@@ -641,7 +650,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   cudaEvent_t e_start = pl->pipe_events[0], e_b = pl->pipe_events[1], e_done = pl->pipe_events[2];
   cudaEvent_t* e_a = &pl->pipe_events[3];
   cudaEvent_t* e_c = &pl->pipe_events[3 + ns];
-  const int64_t m = pl->m, h = m / ns;
+  const int64_t m = pl->m;
   const int P = pl->P;
   // prior work on the call's stream (which may still read the plan buffers) first
   MF_CUDA(cudaEventRecord(e_start, s), "event");
@@ -650,10 +659,11 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, pl->h2d), "H2D B");
   MF_CUDA(cudaEventRecord(e_b, pl->h2d), "event");
   for (int r = 0; r < ns; ++r) {
+    const Rows sr = slab_rows(*pl, r, ns);
     for (int br = 0; br < P; ++br) {
-      const int64_t row = br * m + r * h;
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8, h,
-                                cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
+      const int64_t row = br * m + sr.r0;
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
+                                sr.r1 - sr.r0, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
     }
     MF_CUDA(cudaEventRecord(e_a[r], pl->h2d), "event");
   }
@@ -663,7 +673,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   MF_CUDA(cudaStreamWaitEvent(s, e_b, 0), "wait");
   if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, s), "pre-add B (K4)");
   for (int r = 0; r < ns; ++r) {
-    const Rows rows{r * h, (r + 1) * h};
+    const Rows rows = slab_rows(*pl, r, ns);
     MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
     if (pl->levels == 0) {
       if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, s, rows)) != MF_OK)
@@ -677,9 +687,9 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     MF_CUDA(cudaEventRecord(e_c[r], s), "event");
     MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_c[r], 0), "wait");
     for (int br = 0; br < P; ++br) {
-      const int64_t row = br * m + r * h;
-      MF_CUDA(cudaMemcpy2DAsync(C + row * ldc, ldc * 8, dC + row * n, n * 8, n * 8, h,
-                                cudaMemcpyDeviceToHost, pl->d2h), "D2H C slab");
+      const int64_t row = br * m + rows.r0;
+      MF_CUDA(cudaMemcpy2DAsync(C + row * ldc, ldc * 8, dC + row * n, n * 8, n * 8,
+                                rows.r1 - rows.r0, cudaMemcpyDeviceToHost, pl->d2h), "D2H C slab");
     }
   }
   MF_CUDA(cudaEventRecord(e_done, pl->d2h), "event");
