@@ -35,6 +35,7 @@
 //    a product are rasterised in groups of 8 tile-rows for L2 reuse.
 #include <cuda.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -43,14 +44,13 @@
 namespace mf {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int BM = 128, BN = 128, BK = 16;  // BN: the default (widest) tile
 constexpr int STAGES = 5;
 constexpr int MMA_WARPS = 8;
 constexpr int THREADS = MMA_WARPS * 32;
 constexpr int A_BYTES = BM * BK * 8;
-constexpr int B_BYTES = BK * BN * 8;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+template <int BNT> __host__ __device__ constexpr int stage_bytes() { return A_BYTES + BK * BNT * 8; }
+template <int BNT> __host__ __device__ constexpr int smem_bytes() { return STAGES * stage_bytes<BNT>() + 2 * STAGES * 8 + 1024; }
 constexpr int GROUP_M = 8;
 
 // B-tile staging modes (all TMA):
@@ -137,10 +137,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
+// BNT = CTA tile width (128, or 64 to cut wave quantisation on small batches):
+// warps form a 2 x 4 grid of 64 x (BNT/4) warp tiles, NJ = BNT/64 16-column
+// groups per warp.
+template <int BNT>
 __global__ void __launch_bounds__(THREADS, 1)
 leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
                  const LeafParams prm) {
+  constexpr int NJ = BNT / 64, WN = BNT / 4;
+  constexpr int STAGE_BYTES = stage_bytes<BNT>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -186,16 +192,16 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     else      tma_load_4d(dA, mapA, fb, kb * BK, a_bc, tm * BM, a_br);
     if (prm.bmode == B_BOXES) {
 #pragma unroll
-      for (int j = 0; j < BN / 16; ++j) {
-        if (b_ws) tma_load_3d(dB + j * 2048, mapB, fb, tn * BN + 16 * j, kb * BK, job.b_coord);
-        else      tma_load_4d(dB + j * 2048, mapB, fb, tn * BN + 16 * j, b_bc, kb * BK, b_br);
+      for (int j = 0; j < BNT / 16; ++j) {
+        if (b_ws) tma_load_3d(dB + j * 2048, mapB, fb, tn * BNT + 16 * j, kb * BK, job.b_coord);
+        else      tma_load_4d(dB + j * 2048, mapB, fb, tn * BNT + 16 * j, b_bc, kb * BK, b_br);
       }
     } else if (prm.bmode == B_5D) {
-      if (b_ws) tma_load_4d(dB, mapB, fb, 0, kb * BK, tn * (BN / 16), job.b_coord);
-      else      tma_load_5d(dB, mapB, fb, 0, kb * BK, tn * (BN / 16), b_bc, b_br);
+      if (b_ws) tma_load_4d(dB, mapB, fb, 0, kb * BK, tn * (BNT / 16), job.b_coord);
+      else      tma_load_5d(dB, mapB, fb, 0, kb * BK, tn * (BNT / 16), b_bc, b_br);
     } else {
-      if (b_ws) tma_load_3d(dB, mapB, fb, tn * BN, kb * BK, job.b_coord);
-      else      tma_load_4d(dB, mapB, fb, tn * BN, b_bc, kb * BK, b_br);
+      if (b_ws) tma_load_3d(dB, mapB, fb, tn * BNT, kb * BK, job.b_coord);
+      else      tma_load_4d(dB, mapB, fb, tn * BNT, b_bc, kb * BK, b_br);
     }
   };
   if (threadIdx.x == 0) {
@@ -209,11 +215,11 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int wn = warp & 3;   // 0..3 -> 32-col quarter
   const int lr = lane >> 2, lk = lane & 3;
 
-  double acc[8][2][2][2];
+  double acc[8][NJ][2][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int u = 0; u < 2; ++u) { acc[i][j][u][0] = 0.0; acc[i][j][u][1] = 0.0; }
 
@@ -229,11 +235,11 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   for (int s2 = 0; s2 < 2; ++s2) {
     const uint32_t r0 = 2 * c0 + s2, r1 = 2 * c1 + s2;  // B rows (k) for g = 0, 1
     if (prm.bmode == B_ROWS) {
-      offB[0][s2] = r0 * (BN * 8) + (wn * 32 + 2 * lr) * 8;
-      offB[1][s2] = r1 * (BN * 8) + (wn * 32 + 2 * lr) * 8;
+      offB[0][s2] = r0 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
+      offB[1][s2] = r1 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
     } else {
-      offB[0][s2] = (2 * wn) * 2048 + r0 * 128 + ((lr ^ (r0 & 7)) << 4);
-      offB[1][s2] = (2 * wn) * 2048 + r1 * 128 + ((lr ^ (r1 & 7)) << 4);
+      offB[0][s2] = (NJ * wn) * 2048 + r0 * 128 + ((lr ^ (r0 & 7)) << 4);
+      offB[1][s2] = (NJ * wn) * 2048 + r1 * 128 + ((lr ^ (r1 & 7)) << 4);
     }
   }
   nj_stride = prm.bmode == B_ROWS ? 16 * 8 : 2048;
@@ -242,23 +248,23 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   // DMMAs, so no k-group starts on an LDS-latency bubble.  A stage's slot is
   // released (mbarrier.arrive has release semantics: the LDS reads are
   // complete) as soon as its last fragment load has been issued.
-  double fa0[8][2], fb0[2][2][2], fa1[8][2], fb1[2][2][2];
-  auto load_frags = [&](uint32_t sA, uint32_t sB, int g, double (&fa)[8][2], double (&fb)[2][2][2]) {
+  double fa0[8][2], fb0[NJ][2][2], fa1[8][2], fb1[NJ][2][2];
+  auto load_frags = [&](uint32_t sA, uint32_t sB, int g, double (&fa)[8][2], double (&fb)[NJ][2][2]) {
 #pragma unroll
     for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, fa[mi][0], fa[mi][1]);
 #pragma unroll
-    for (int nj = 0; nj < 2; ++nj)
+    for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2)
         lds128(sB + offB[g][s2] + nj * nj_stride, fb[nj][s2][0], fb[nj][s2][1]);
   };
-  auto mma_group = [&](const double (&fa)[8][2], const double (&fb)[2][2][2]) {
+  auto mma_group = [&](const double (&fa)[8][2], const double (&fb)[NJ][2][2]) {
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 2; ++nj)
+        for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
           for (int j = 0; j < 2; ++j)
             dmma(acc[mi][nj][j][0], acc[mi][nj][j][1], fa[mi][s2], fb[nj][s2][j]);
@@ -300,8 +306,8 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
     if (row >= prm.m) continue;
 #pragma unroll
-    for (int nj = 0; nj < 2; ++nj) {
-      const int64_t col = (int64_t)tn * BN + wn * 32 + nj * 16 + 4 * lk;
+    for (int nj = 0; nj < NJ; ++nj) {
+      const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
       double v0 = acc[mi][nj][0][0], v1 = acc[mi][nj][1][0];
       double v2 = acc[mi][nj][0][1], v3 = acc[mi][nj][1][1];
       if (alpha != 1.0) {
@@ -468,18 +474,39 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
            encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, BN, BK,
                             CU_TENSOR_MAP_SWIZZLE_NONE);
     if (!ok) return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(leaf_dmma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    // Tile width: 64 when 128-wide tiles would leave a badly filled last wave
+    // (e.g. 7 products of 2048^2: 12.1 waves of 148 SMs) -- model: wave fill
+    // times a 2% per-tile penalty for the narrower tile (MF_LEAF_BN overrides).
+    const int64_t tm_tiles = (r1 - r0 + BM - 1) / BM;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    auto fill = [&](int bn) {
+      const double waves = (double)(tm_tiles * ((a.m + bn - 1) / bn) * a.n_jobs) / sms;
+      return waves / std::ceil(waves);
+    };
+    int bn = (bmode == B_ROWS && fill(64) * 0.98 > fill(128)) ? 64 : 128;
+    if (const char* e = getenv("MF_LEAF_BN")) bn = atoi(e) == 64 && bmode == B_ROWS ? 64 : 128;
+    if (bn == 64) {  // re-encode B with 64-wide boxes
+      ok = encode_block_view(&mB, a.B, a.ldb, a.P, a.m, 64, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, 64, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (!ok) return cudaErrorInvalidValue;
+    }
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[bn == 64]) {
+      cudaError_t e = bn == 64
+          ? cudaFuncSetAttribute(leaf_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes<64>())
+          : cudaFuncSetAttribute(leaf_dmma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes<128>());
       if (e != cudaSuccess) return e;
-      attr_set = true;
+      attr_set[bn == 64] = true;
     }
     LeafParams prm;
     prm.m = a.m;
     prm.tm0 = (int)(r0 / BM);
-    prm.tiles_m = (int)((r1 - r0 + BM - 1) / BM);
-    prm.tiles_n = (int)((a.m + BN - 1) / BN);
+    prm.tiles_m = (int)tm_tiles;
+    prm.tiles_n = (int)((a.m + bn - 1) / bn);
     prm.kblocks = (int)((a.m + BK - 1) / BK);
     prm.bmode = bmode;
     prm.out = a.out;
@@ -489,7 +516,10 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.jobs = a.jobs;
     const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
-    leaf_dmma_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mA, mT, mB, mS, prm);
+    if (bn == 64)
+      leaf_dmma_kernel<64><<<(unsigned)grid, THREADS, smem_bytes<64>(), s>>>(mA, mT, mB, mS, prm);
+    else
+      leaf_dmma_kernel<128><<<(unsigned)grid, THREADS, smem_bytes<128>(), s>>>(mA, mT, mB, mS, prm);
     return cudaGetLastError();
   }
   SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, a.out, a.ldo,
