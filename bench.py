@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-classical", action="store_true")
+    ap.add_argument("--level-by-level", action="store_true",
+                    help="ablation: the paper's recursion instead of the flattened triple")
     a = ap.parse_args()
     if a.config:
         a.n, a.triple, a.levels = CONFIGS[a.config]
@@ -75,7 +77,8 @@ def parse():
 
 
 def workload_name(a):
-    return f"n={a.n} fp64, {a.levels}-level {a.triple} (flattened, {_rank(a) ** a.levels} leaf products)"
+    mode = "level by level" if getattr(a, "level_by_level", False) else "flattened"
+    return f"n={a.n} fp64, {a.levels}-level {a.triple} ({mode}, {_rank(a) ** a.levels} leaf products)"
 
 
 def _rank(a):
@@ -234,7 +237,7 @@ def main():
     n = a.n
     triple = mf.triples.get(a.triple)
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
-                   nccl_comm=comm, profile=True)
+                   nccl_comm=comm, profile=True, level_by_level=a.level_by_level)
     info = plan.info()
     stream = torch.cuda.current_stream()
     A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
@@ -274,6 +277,9 @@ def main():
     m = info["leaf_n"]
     leaf_ms = phases["leaf"] / max(1, phases["calls"])
     leaf_flops = my_prods * 2.0 * m ** 3
+    if a.level_by_level:  # the leaf phase holds the whole sub-recursion of each product
+        R, p = _rank(a), {"laderman": 3}.get(a.triple, 2)
+        leaf_flops = R ** a.levels * 2.0 * (n // p ** a.levels) ** 3
     peak, peak_src = fp64_peak()
     achieved = leaf_flops / (leaf_ms * 1e-3) / 1e12
     roofline = {"bound": "tensor", "kernel": "leaf_dmma_kernel (K5)", "achieved": achieved,
@@ -286,7 +292,8 @@ def main():
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config(a, world), "clocks": clk,
-           "gpu_launches": 4 * a.steps if a.levels > 0 else a.steps,
+           "gpu_launches": (4 if a.levels > 0 else 1) * a.steps if not a.level_by_level
+                           else (2 + _rank(a) * 4 + 1) * a.steps,
            "roofline": roofline}
 
     # ---- accuracy vs classical cuBLAS DGEMM, and the classical baselines ----

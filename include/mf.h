@@ -73,6 +73,13 @@ typedef struct {
                            classification, sharding) -- no device, no workspace;
                            mf_plan_info / mf_plan_products work, compute calls
                            return MF_ERR_INVALID_ARG                              */
+  int32_t level_by_level; /* 0 (default): run `levels` as ONE level of the
+                           Kronecker-flattened triple.  1: the paper's recursion
+                            -- one level of <U,V,W> whose R leaf
+                           products are each a (levels-1)-level product; same
+                           bilinear map, more HBM passes (an ablation).  With 1,
+                           mf_plan_info / mf_plan_products describe the top
+                           level (R products, leaf_n = n / p)                    */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.

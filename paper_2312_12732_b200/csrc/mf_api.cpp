@@ -309,6 +309,28 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     P *= p;
     RL *= R;
   }
+  if (o.level_by_level && levels >= 2) {
+    // the paper's recursion: this plan = one level; each of its R products is
+    // computed by a child plan of levels - 1 levels at n / p
+    mf_options top = o, sub = o;
+    top.level_by_level = 0;
+    sub.shard_rank = 0; sub.shard_count = 1; sub.nccl_comm = nullptr; sub.profile = 0;
+    sub.input_mode = MF_IN_REPLICATED;
+    mf_plan_t parent = nullptr, child = nullptr;
+    mf_status st = mf_plan(&parent, p, R, U, V, W, 1, n, &top);
+    if (st != MF_OK) return st;
+    st = mf_plan(&child, p, R, U, V, W, levels - 1, n / p, &sub);
+    if (st != MF_OK) {
+      std::string msg = g_err;
+      mf_destroy(parent);
+      g_err = msg;
+      return st;
+    }
+    parent->child = child;
+    parent->opt.level_by_level = 1;
+    *out = parent;
+    return MF_OK;
+  }
   if (P > 256 || RL > (1 << 20))
     return fail(MF_ERR_UNSUPPORTED, "flattened triple too large (p^levels = %lld, R^levels = %lld)",
                 (long long)P, (long long)RL);
@@ -453,6 +475,7 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
 mf_status mf_destroy(mf_plan_t plan) {
   g_err.clear();
   if (!plan) return MF_OK;
+  if (plan->child) mf_destroy(static_cast<mf_plan_t>(plan->child));
   free_plan(plan);
   delete plan;
   return MF_OK;
@@ -546,9 +569,30 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
     mark(1);
     MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
     mark(2);
-    // a3: all leaf products in one launch (K5)
-    if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) != MF_OK)
-      return st;
+    if (pl->child) {
+      // a5: level by level -- each product P_q' = X_q Y_q is itself computed by
+      // the (levels-1)-level child plan ("recursively solve P_i")
+      const int64_t m = pl->m, mm = m * m;
+      for (int32_t q : pl->my_prods) {
+        const Product& pr = pl->prods[q];
+        const double* X = pr.a_src == SRC_WORKSPACE
+                              ? pl->T + (int64_t)pr.a_idx * mm
+                              : A + (int64_t)(pr.a_idx / pl->P) * m * lda + (pr.a_idx % pl->P) * m;
+        const double* Y = pr.b_src == SRC_WORKSPACE
+                              ? pl->S + (int64_t)pr.b_idx * mm
+                              : B + (int64_t)(pr.b_idx / pl->P) * m * ldb + (pr.b_idx % pl->P) * m;
+        const int64_t ldx = pr.a_src == SRC_WORKSPACE ? m : lda;
+        const int64_t ldy = pr.b_src == SRC_WORKSPACE ? m : ldb;
+        if ((st = mf_dgemm(static_cast<mf_plan_t>(pl->child), 1.0, X, ldx, Y, ldy,
+                           pl->Pw + (int64_t)q * mm, m, stream)) != MF_OK)
+          return st;
+      }
+    } else {
+      // a3: all leaf products in one launch (K5)
+      if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) !=
+          MF_OK)
+        return st;
+    }
     mark(3);
     // a4: fused post-addition (K6)
     MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
@@ -597,7 +641,7 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 // Slab r covers tile rows [r*tm/ns, (r+1)*tm/ns) of 128 rows (the last slab
 // ends at m), so any m with >= 2 tile rows pipelines.
 static int pipeline_slabs(const Plan& pl) {
-  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA) return 1;
+  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child) return 1;
   const int64_t tiles = (pl.m + 127) / 128;
   return (int)std::min<int64_t>(8, tiles);
 }

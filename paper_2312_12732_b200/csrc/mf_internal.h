@@ -91,6 +91,9 @@ struct Plan {
   // NCCL
   void* nccl_comm = nullptr;
   cudaEvent_t done = nullptr;
+  // level-by-level recursion (mf_options.level_by_level): the plan of each
+  // leaf product (levels - 1 levels at n / p); this plan is then one level
+  Plan* child = nullptr;
   // host-buffer pipeline (mf_dgemm_host): copy streams and per-slab events
   cudaStream_t h2d = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> pipe_events;

@@ -202,6 +202,24 @@ def test_dgemm_random_within_bound(name, levels, n):
     assert scaled(C, Co, A, B) <= 1e-13 * max(1, levels)
 
 
+@pytest.mark.parametrize("name,levels,n", [(SW, 2, 256), (SW, 3, 512), ("laderman", 2, 288),
+                                           ("paper-strassen", 2, 512), (SW, 2, 1000)])
+def test_level_by_level_recursion(name, levels, n):
+    """a5: the paper's recursion executed level by level -- the
+    same bilinear map as the flattened default: exact on integers; on random
+    inputs within the bound, and close to the oracle's own recursion."""
+    t = triples.get(name)
+    A, B = mf_inputs.pair("int1024", n, 17)
+    with mf.Plan(t, levels, n, level_by_level=True) as p:
+        assert p.info()["n_products"] == t.R and p.info()["leaf_n"] == n // t.p
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 18)
+        C = host(p.dgemm(dev(A), dev(B), alpha=1.5))
+    Co = oracle.fmm(A, B, oracle.catalog(name), levels, alpha=1.5)
+    assert scaled(C, Co, A, B) <= 1e-13 * levels
+    assert scaled(C, 1.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
+
+
 def test_config1_n64_sw1_all_distributions():
     """BASELINE config 1: n=64, one-level Strassen-Winograd."""
     for kind in ("int8", "int1024"):
