@@ -633,25 +633,27 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
   return MF_OK;
 }
 
-// Host-buffer pipeline: B is copied first and pre-added, then
-// the path runs slab by slab over row ranges [r*h, (r+1)*h) of every block:
-// H2D of A's slab r (copy stream) -> K4(A) / K5 / K6 on those rows (the call's
-// stream) -> D2H of C's slab r (second copy stream), so the PCIe transfers of
-// slab r+1 and r-1 overlap the compute of slab r.
-// Slab r covers tile rows [r*tm/ns, (r+1)*tm/ns) of 128 rows (the last slab
-// ends at m), so any m with >= 2 tile rows pipelines.
+// Host-buffer pipeline.  The leaf of output rows r needs A's
+// row slab r (of every block) and all of B; its columns c need only B's
+// column slab c.  Schedule (copy stream h2d, the call's stream s, copy stream
+// d2h):
+//   h2d: A slabs 0..H-1, then B column slabs 0..NC-1, then A slabs H..NS-1;
+//   s:   for each column slab c: K4(B) on it, then for the first H row slabs
+//        K4(A) (once), K5 and K6 on region (r, c); then row slabs H..NS-1
+//        whole: K4(A), K5, K6;
+//   d2h: each finished C region, as soon as it is done.
+// Compute starts after ~(H/NS + 1/NC) of the inputs crossed PCIe and the
+// remaining copies overlap compute; results are bitwise those of mf_dgemm.
 static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child) return 1;
   const int64_t tiles = (pl.m + 127) / 128;
   return (int)std::min<int64_t>(8, tiles);
 }
 
-static Rows slab_rows(const Plan& pl, int r, int ns) {
-  const int64_t tiles = (pl.m + 127) / 128;
-  Rows rows;
-  rows.r0 = std::min<int64_t>(pl.m, 128 * (r * tiles / ns));
-  rows.r1 = std::min<int64_t>(pl.m, 128 * ((r + 1) * tiles / ns));
-  return rows;
+// piece i of n over the 128-aligned tiles of [0, m)
+static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n) {
+  const int64_t tiles = (m + 127) / 128;
+  return {std::min<int64_t>(m, 128 * (i * tiles / n)), std::min<int64_t>(m, 128 * ((i + 1) * tiles / n))};
 }
 
 mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
@@ -683,58 +685,105 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return MF_OK;
   }
+  const int64_t m = pl->m;
+  const int P = pl->P;
+  const int nc = (int)std::min<int64_t>(4, (m + 127) / 128);  // B column slabs
+  const int head = std::min(2, ns);                            // row slabs done column-wise
   if (!pl->h2d) MF_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking), "stream");
   if (!pl->d2h) MF_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking), "stream");
-  const size_t nev = 3 + 2 * ns;  // start, B ready, done, A slab r ready, C slab r ready
+  const size_t nev = 3 + ns + nc + (size_t)head * nc + ns;
   while (pl->pipe_events.size() < nev) {
     cudaEvent_t e;
     MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     pl->pipe_events.push_back(e);
   }
-  cudaEvent_t e_start = pl->pipe_events[0], e_b = pl->pipe_events[1], e_done = pl->pipe_events[2];
+  cudaEvent_t e_start = pl->pipe_events[0], e_done = pl->pipe_events[1];
   cudaEvent_t* e_a = &pl->pipe_events[3];
-  cudaEvent_t* e_c = &pl->pipe_events[3 + ns];
-  const int64_t m = pl->m;
-  const int P = pl->P;
+  cudaEvent_t* e_b = e_a + ns;
+  cudaEvent_t* e_c = e_b + nc;
+  int next_c = 0;
+  const double* dA = pl->hA;
+  const double* dB = pl->hB;
+  double* dC = pl->hC;
+
+  auto h2d_a_slab = [&](int r) -> mf_status {
+    const auto sr = tile_piece(m, r, ns);
+    for (int br = 0; br < P; ++br) {
+      const int64_t row = br * m + sr.first;
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
+                                sr.second - sr.first, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
+    }
+    MF_CUDA(cudaEventRecord(e_a[r], pl->h2d), "event");
+    return MF_OK;
+  };
+  // compute + D2H of one region of every C block
+  auto region = [&](Rows rg) -> mf_status {
+    if (pl->levels == 0) {
+      if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, s, rg)) != MF_OK) return st;
+    } else {
+      if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, rg)) != MF_OK)
+        return st;
+      MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, dC, n, s, rg), "post-add (K6)");
+    }
+    cudaEvent_t ev = e_c[next_c++];
+    MF_CUDA(cudaEventRecord(ev, s), "event");
+    MF_CUDA(cudaStreamWaitEvent(pl->d2h, ev, 0), "wait");
+    const int64_t r0 = rg.r0, r1 = rg.end(m), c0 = rg.c0, c1 = rg.cend(m);
+    for (int br = 0; br < P; ++br)
+      for (int bc = 0; bc < P; ++bc) {
+        const int64_t off = bc * m + c0;  // column offset of block (br, bc)'s region
+        MF_CUDA(cudaMemcpy2DAsync(C + (br * m + r0) * ldc + off, ldc * 8, dC + (br * m + r0) * n + off,
+                                  n * 8, (c1 - c0) * 8, r1 - r0, cudaMemcpyDeviceToHost, pl->d2h),
+                "D2H C region");
+      }
+    return MF_OK;
+  };
+
   // prior work on the call's stream (which may still read the plan buffers) first
   MF_CUDA(cudaEventRecord(e_start, s), "event");
   MF_CUDA(cudaStreamWaitEvent(pl->h2d, e_start, 0), "wait");
   MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_start, 0), "wait");
-  MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, pl->h2d), "H2D B");
-  MF_CUDA(cudaEventRecord(e_b, pl->h2d), "event");
-  for (int r = 0; r < ns; ++r) {
-    const Rows sr = slab_rows(*pl, r, ns);
-    for (int br = 0; br < P; ++br) {
-      const int64_t row = br * m + sr.r0;
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
-                                sr.r1 - sr.r0, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
-    }
-    MF_CUDA(cudaEventRecord(e_a[r], pl->h2d), "event");
+  for (int r = 0; r < head; ++r)
+    if ((st = h2d_a_slab(r)) != MF_OK) return st;
+  for (int c = 0; c < nc; ++c) {
+    const auto sc = tile_piece(m, c, nc);
+    for (int bc = 0; bc < P; ++bc)
+      MF_CUDA(cudaMemcpy2DAsync(pl->hB + bc * m + sc.first, n * 8, B + bc * m + sc.first, ldb * 8,
+                                (sc.second - sc.first) * 8, n, cudaMemcpyHostToDevice, pl->h2d),
+              "H2D B column slab");
+    MF_CUDA(cudaEventRecord(e_b[c], pl->h2d), "event");
   }
-  const double* dA = pl->hA;
-  const double* dB = pl->hB;
-  double* dC = pl->hC;
-  MF_CUDA(cudaStreamWaitEvent(s, e_b, 0), "wait");
-  if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, s), "pre-add B (K4)");
-  for (int r = 0; r < ns; ++r) {
-    const Rows rows = slab_rows(*pl, r, ns);
+  for (int r = head; r < ns; ++r)
+    if ((st = h2d_a_slab(r)) != MF_OK) return st;
+
+  for (int c = 0; c < nc; ++c) {
+    const auto sc = tile_piece(m, c, nc);
+    MF_CUDA(cudaStreamWaitEvent(s, e_b[c], 0), "wait");
+    if (pl->levels > 0) {
+      Rows cols;
+      cols.c0 = sc.first; cols.c1 = sc.second;
+      MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, s, cols), "pre-add B (K4)");
+    }
+    for (int r = 0; r < head; ++r) {
+      const auto sr = tile_piece(m, r, ns);
+      if (c == 0) {
+        MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
+        Rows rows;
+        rows.r0 = sr.first; rows.r1 = sr.second;
+        if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
+      }
+      Rows rg;
+      rg.r0 = sr.first; rg.r1 = sr.second; rg.c0 = sc.first; rg.c1 = sc.second;
+      if ((st = region(rg)) != MF_OK) return st;
+    }
+  }
+  for (int r = head; r < ns; ++r) {
+    const auto sr = tile_piece(m, r, ns);
     MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
-    if (pl->levels == 0) {
-      if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, s, rows)) != MF_OK)
-        return st;
-    } else {
-      MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
-      if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, rows)) != MF_OK)
-        return st;
-      MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, dC, n, s, rows), "post-add (K6)");
-    }
-    MF_CUDA(cudaEventRecord(e_c[r], s), "event");
-    MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_c[r], 0), "wait");
-    for (int br = 0; br < P; ++br) {
-      const int64_t row = br * m + rows.r0;
-      MF_CUDA(cudaMemcpy2DAsync(C + row * ldc, ldc * 8, dC + row * n, n * 8, n * 8,
-                                rows.r1 - rows.r0, cudaMemcpyDeviceToHost, pl->d2h), "D2H C slab");
-    }
+    Rows rows;
+    rows.r0 = sr.first; rows.r1 = sr.second;
+    if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
+    if ((st = region(rows)) != MF_OK) return st;
   }
   MF_CUDA(cudaEventRecord(e_done, pl->d2h), "event");
   MF_CUDA(cudaStreamWaitEvent(s, e_done, 0), "wait");  // keep the call's stream ordered after D2H

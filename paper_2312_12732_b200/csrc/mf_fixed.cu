@@ -203,15 +203,16 @@ __device__ __forceinline__ void premix_all(const V<VW> (&x)[P * P], double* out,
 template <class Tag, int SIDE, int P, int R, int VW>
 __global__ void __launch_bounds__(256) premix_fixed(const double* __restrict__ X, int64_t ldx,
                                                     int64_t m, double* __restrict__ out,
-                                                    int64_t r0, int64_t r1) {
+                                                    int64_t r0, int64_t r1, int64_t c0,
+                                                    int64_t c1) {
   constexpr int NB = P * P;
-  const int64_t vpr = m / VW;
+  const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = r0 + idx / vpr;
-    const int64_t c = (idx % vpr) * VW;
+    const int64_t c = c0 + (idx % vpr) * VW;
     V<VW> x[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) x[k] = ld_stream<VW>(X + ((k / P) * m + r) * ldx + (k % P) * m + c);
@@ -241,15 +242,16 @@ __device__ __forceinline__ void postmix_all(V<VW> (&acc)[P * P], const double* _
 template <class Tag, int P, int R, int VW>
 __global__ void __launch_bounds__(256) postmix_fixed(const double* __restrict__ Pw, int64_t m,
                                                      double alpha, double* __restrict__ C,
-                                                     int64_t ldc, int64_t r0, int64_t r1) {
+                                                     int64_t ldc, int64_t r0, int64_t r1,
+                                                     int64_t c0, int64_t c1) {
   constexpr int NB = P * P;
-  const int64_t vpr = m / VW;
+  const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = r0 + idx / vpr;
-    const int64_t c = (idx % vpr) * VW;
+    const int64_t c = c0 + (idx % vpr) * VW;
     V<VW> acc[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i)
@@ -289,18 +291,20 @@ bool equal(const Tri<NB, R>& t, const Plan& pl) {
 
 template <class Tag, int P, int R, int VW>
 cudaError_t run_premix(int side, const double* X, int64_t ldx, int64_t m, double* out,
-                       cudaStream_t s, int64_t r0, int64_t r1) {
-  const int grid = grid_for((r1 - r0) * (m / VW));
-  if (side == 0) premix_fixed<Tag, 0, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1);
-  else premix_fixed<Tag, 1, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1);
+                       cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  const int grid = grid_for((r1 - r0) * ((c1 - c0) / VW));
+  if (side == 0)
+    premix_fixed<Tag, 0, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1);
+  else
+    premix_fixed<Tag, 1, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1);
   return cudaGetLastError();
 }
 
 template <class Tag, int P, int R, int VW>
 cudaError_t run_postmix(const double* Pw, int64_t m, double alpha, double* C, int64_t ldc,
-                        cudaStream_t s, int64_t r0, int64_t r1) {
-  postmix_fixed<Tag, P, R, VW><<<grid_for((r1 - r0) * (m / VW)), 256, 0, s>>>(Pw, m, alpha, C, ldc,
-                                                                             r0, r1);
+                        cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+  postmix_fixed<Tag, P, R, VW><<<grid_for((r1 - r0) * ((c1 - c0) / VW)), 256, 0, s>>>(
+      Pw, m, alpha, C, ldc, r0, r1, c0, c1);
   return cudaGetLastError();
 }
 
@@ -342,17 +346,17 @@ bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t 
 
 cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
                                 double* out, cudaStream_t s, Rows rows) {
-  const int64_t r0 = rows.r0, r1 = rows.end(m);
-#define PRE(T_, P_, R_) fixed::run_premix<T_, P_, R_, 4>(side, X, ldx, m, out, s, r0, r1)
+  const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
+#define PRE(T_, P_, R_) fixed::run_premix<T_, P_, R_, 4>(side, X, ldx, m, out, s, r0, r1, c0, c1)
   MF_FIXED_SWITCH(id, PRE)
 #undef PRE
 }
 
 cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
                                  int64_t ldc, cudaStream_t s, Rows rows) {
-  const int64_t r0 = rows.r0, r1 = rows.end(m);
+  const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
 #define POST(T_, P_, R_) \
-  fixed::run_postmix<T_, P_, R_, (P_ >= 4 ? 2 : 4)>(Pw, m, alpha, C, ldc, s, r0, r1)
+  fixed::run_postmix<T_, P_, R_, (P_ >= 4 ? 2 : 4)>(Pw, m, alpha, C, ldc, s, r0, r1, c0, c1)
   MF_FIXED_SWITCH(id, POST)
 #undef POST
 }

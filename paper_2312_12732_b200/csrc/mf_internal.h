@@ -102,11 +102,14 @@ struct Plan {
   size_t prof_used = 0;
 };
 
-// Rows [r0, r1) of every m x m block a launch covers (the whole block by
-// default); the host-buffer pipeline runs the path slab by slab.
+// Region [r0, r1) x [c0, c1) of every m x m block a launch covers (the whole
+// block by default); the host-buffer pipeline runs the path piece by piece.
+// Column bounds are multiples of 64 (or m) -- tile and vector aligned.
 struct Rows {
   int64_t r0 = 0, r1 = -1;  // r1 < 0 => m
+  int64_t c0 = 0, c1 = -1;  // c1 < 0 => m
   int64_t end(int64_t m) const { return r1 < 0 ? m : r1; }
+  int64_t cend(int64_t m) const { return c1 < 0 ? m : c1; }
 };
 
 // ---- launchers (mf_mix.cu, mf_leaf.cu); return cudaError_t of the launch ----

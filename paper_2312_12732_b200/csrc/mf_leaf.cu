@@ -62,7 +62,7 @@ enum BMode : int { B_ROWS = 0, B_BOXES = 1, B_5D = 2 };
 
 struct LeafParams {
   int64_t m;
-  int tm0;  // first tile row (row slab of the host-buffer pipeline)
+  int tm0, tn0;  // first tile row / column (region of the host-buffer pipeline)
   int tiles_m, tiles_n, kblocks;
   int bmode;
   double* out;
@@ -162,7 +162,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int first_m = (t / group_tiles) * GROUP_M;
   const int gsz = min(prm.tiles_m - first_m, GROUP_M);
   const int tm = prm.tm0 + first_m + (t % group_tiles) % gsz;
-  const int tn = (t % group_tiles) / gsz;
+  const int tn = prm.tn0 + (t % group_tiles) / gsz;
   const LeafJob job = prm.jobs[job_id];
 
   const int warp = threadIdx.x >> 5;
@@ -333,7 +333,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 // describe (odd m or odd leading dimension).
 struct SimpleParams {
   const double *A, *B, *T, *S;
-  int64_t lda, ldb, m, r0, r1;
+  int64_t lda, ldb, m, r0, r1, c0, c1;
   double* out;
   int64_t ldo, out_stride;
   double alpha;
@@ -343,8 +343,8 @@ struct SimpleParams {
 __global__ void leaf_simple_kernel(const SimpleParams prm) {
   const LeafJob job = prm.jobs[blockIdx.z];
   const int64_t r = prm.r0 + (int64_t)blockIdx.y * 16 + threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * 16 + threadIdx.x;
-  if (r >= prm.r1 || c >= prm.m) return;
+  const int64_t c = prm.c0 + (int64_t)blockIdx.x * 16 + threadIdx.x;
+  if (r >= prm.r1 || c >= prm.c1) return;
   const int64_t mm = prm.m * prm.m;
   const double* X;
   int64_t ldx;
@@ -445,9 +445,10 @@ bool leaf_tma_supported(const LeafArgs& a) {
 }
 
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
-  const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m);
-  if (a.n_jobs == 0 || a.m == 0 || r1 <= r0) return cudaSuccess;
-  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && r0 % BM == 0) {
+  const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m), c0 = a.rows.c0, c1 = a.rows.cend(a.m);
+  if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cudaSuccess;
+  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && r0 % BM == 0 && c0 % BN == 0 &&
+      (c1 == a.m || c1 % BN == 0)) {
     int bmode = B_ROWS;  // measured fastest (profiles/leaf_bmode_r01.json)
     if (const char* e = getenv("MF_LEAF_BMODE")) bmode = atoi(e);  // experiments: 0, 1, 2
     if (bmode == B_5D && a.m % 16 != 0) bmode = B_BOXES;
@@ -482,7 +483,7 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     auto fill = [&](int bn) {
-      const double waves = (double)(tm_tiles * ((a.m + bn - 1) / bn) * a.n_jobs) / sms;
+      const double waves = (double)(tm_tiles * ((c1 - c0 + bn - 1) / bn) * a.n_jobs) / sms;
       return waves / std::ceil(waves);
     };
     int bn = (bmode == B_ROWS && fill(64) * 0.98 > fill(128)) ? 64 : 128;
@@ -506,7 +507,8 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.m = a.m;
     prm.tm0 = (int)(r0 / BM);
     prm.tiles_m = (int)tm_tiles;
-    prm.tiles_n = (int)((a.m + bn - 1) / bn);
+    prm.tn0 = (int)(c0 / bn);
+    prm.tiles_n = (int)((c1 - c0 + bn - 1) / bn);
     prm.kblocks = (int)((a.m + BK - 1) / BK);
     prm.bmode = bmode;
     prm.out = a.out;
@@ -522,9 +524,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
       leaf_dmma_kernel<128><<<(unsigned)grid, THREADS, smem_bytes<128>(), s>>>(mA, mT, mB, mS, prm);
     return cudaGetLastError();
   }
-  SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, a.out, a.ldo,
+  SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, c0, c1, a.out, a.ldo,
                    a.out_block_stride, a.alpha, a.jobs};
-  dim3 grid((unsigned)((a.m + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), (unsigned)a.n_jobs);
+  dim3 grid((unsigned)((c1 - c0 + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), (unsigned)a.n_jobs);
   leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
   return cudaGetLastError();
 }

@@ -107,7 +107,7 @@ template <int VW>
 __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
                                                   const void* __restrict__ table, int nrow,
                                                   int nterm, double alpha, int64_t r0,
-                                                  int64_t r1) {
+                                                  int64_t r1, int64_t c0, int64_t c1) {
   extern __shared__ __align__(16) uint8_t s_raw[];
   const size_t tbytes = sizeof(MixRow) * nrow + sizeof(MixTerm) * nterm;
   for (size_t i = threadIdx.x; i < tbytes / 8; i += blockDim.x)
@@ -117,12 +117,12 @@ __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
   const MixTerm* terms = reinterpret_cast<const MixTerm*>(rows + nrow);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int SEG = 32 * VW;
-  const int64_t segs_per_row = (m + SEG - 1) / SEG;
+  const int64_t segs_per_row = (c1 - c0 + SEG - 1) / SEG;
   const int64_t total = (r1 - r0) * segs_per_row;
   for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
     const int64_t r = r0 + seg / segs_per_row;
-    const int64_t c = (seg % segs_per_row) * SEG + lane * VW;
-    if (c >= m) continue;
+    const int64_t c = c0 + (seg % segs_per_row) * SEG + lane * VW;
+    if (c >= c1) continue;
     for (int o = warp; o < nrow; o += 8) {
       const MixRow row = rows[o];
       Vec<VW> acc;
@@ -164,15 +164,15 @@ int grid_for(int64_t work, int per_block) {
 
 template <int VW>
 cudaError_t mix_launch(const MixTable& t, View in, View out, int64_t m, double alpha, cudaStream_t s,
-                       int64_t r0, int64_t r1) {
+                       int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
   const size_t smem = sizeof(MixRow) * t.nrow + sizeof(MixTerm) * t.nterm;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(mix_kernel<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  mix_kernel<VW><<<grid_for((r1 - r0) * ((m + 32 * VW - 1) / (32 * VW)), 1), 256, smem, s>>>(
-      in, out, m, t.d_table, t.nrow, t.nterm, alpha, r0, r1);
+  mix_kernel<VW><<<grid_for((r1 - r0) * ((c1 - c0 + 32 * VW - 1) / (32 * VW)), 1), 256, smem, s>>>(
+      in, out, m, t.d_table, t.nrow, t.nterm, alpha, r0, r1, c0, c1);
   return cudaGetLastError();
 }
 
@@ -196,16 +196,16 @@ static int pick_vw(int64_t m, std::initializer_list<std::pair<const void*, int64
 static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, int64_t m,
                                 double alpha, cudaStream_t s, Rows rows) {
   if (t.nrow == 0) return cudaSuccess;
-  const int64_t r0 = rows.r0, r1 = rows.end(m);
-  if (r1 <= r0) return cudaSuccess;
-  if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s, r0, r1);
-  if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s, r0, r1);
-  return mix_launch<1>(t, in, out, m, alpha, s, r0, r1);
+  const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
+  if (r1 <= r0 || c1 <= c0) return cudaSuccess;
+  if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s, r0, r1, c0, c1);
+  if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s, r0, r1, c0, c1);
+  return mix_launch<1>(t, in, out, m, alpha, s, r0, r1, c0, c1);
 }
 
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows) {
-  if (t.nrow == 0 || rows.end(pl.m) <= rows.r0) return cudaSuccess;
+  if (t.nrow == 0 || rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
   if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
     return launch_premix_fixed(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s, rows);
   const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
@@ -215,7 +215,7 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
 
 cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C, int64_t ldc,
                            cudaStream_t s, Rows rows) {
-  if (rows.end(pl.m) <= rows.r0) return cudaSuccess;
+  if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
   if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
     return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
