@@ -138,9 +138,16 @@ mf_status mf_plan_info(mf_plan_t plan, size_t* workspace_bytes, int64_t* leaf_n,
  * of the T workspace; b_src/b_idx likewise for B and S; sign[q] = +-1, the
  * sign folded out of aliased operands (P_q as produced by the leaf stage is
  * sign[q] times the P_q of Eq. "strassen"); shard[q] = the shard that computes
- * product q. */
+ * product q whole, or -1 for a product split by rows across all shards. */
 mf_status mf_plan_products(mf_plan_t plan, int32_t* a_src, int32_t* a_idx, int32_t* b_src,
                            int32_t* b_idx, int32_t* sign, int32_t* shard);
+
+/* Product sharding: with shard_count = N, rank r computes
+ * floor(R^L / N) whole products (a contiguous range) and, of each of the
+ * R^L mod N leftover products (shard[q] = -1), the 128-aligned output row slab
+ * [*r0, *r1) -- exact balance.  Leftovers go whole to ranks when m has fewer
+ * than N tile rows (or for level-by-level plans); then *r0 = *r1 = 0. */
+mf_status mf_plan_shard_rows(mf_plan_t plan, int64_t* r0, int64_t* r1);
 
 /* Component entry points (the steps of mf_dgemm, exposed for step-by-step
  * parity tests against the oracle; stream-ordered, device pointers):

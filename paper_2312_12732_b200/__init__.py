@@ -39,7 +39,8 @@ OUT_ROOT, OUT_ALL = 0, 1
 
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
-           "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read")
+           "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
+           "mf_plan_shard_rows")
 
 
 class mf_options(ctypes.Structure):
@@ -63,6 +64,7 @@ _lib.mf_version.restype = ctypes.c_char_p
 _lib.mf_plan_info.argtypes = [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(_I64),
                               ctypes.POINTER(_I64), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
 _lib.mf_plan_products.argtypes = [_P] * 7
+_lib.mf_plan_shard_rows.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
 _lib.mf_premix.argtypes = [_P, _I32, _P, _I64, _P, _P]
 _lib.mf_leaf.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _P, _P]
 _lib.mf_postmix.argtypes = [_P, _D, _P, _P, _I64, _P]
@@ -167,6 +169,12 @@ class Plan:
         out = dict(zip(self.PHASES, list(ms)))
         out["calls"] = calls.value
         return out
+
+    def shard_rows(self) -> tuple:
+        """Row slab [r0, r1) this rank computes of each split product (0, 0 if none)."""
+        r0, r1 = _I64(), _I64()
+        _check(_lib.mf_plan_shard_rows(self._h, ctypes.byref(r0), ctypes.byref(r1)))
+        return r0.value, r1.value
 
     # -- the hot path ------------------------------------------------------------
     def dgemm(self, A, B, C=None, alpha: float = 1.0, stream=None):

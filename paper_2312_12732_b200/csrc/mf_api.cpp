@@ -221,7 +221,8 @@ void free_plan(Plan* pl) {
   DeviceGuard g(pl->device);
   cudaDeviceSynchronize();
   for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_table,
-                  (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->hA, (void*)pl->hB,
+                  (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
+                  (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
@@ -252,13 +253,14 @@ bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_
 
 mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
                    const double* T, const double* S, double* out, int64_t ldo, int64_t stride,
-                   double alpha, cudaStream_t s, Rows rows = Rows()) {
+                   double alpha, cudaStream_t s, Rows rows = Rows(), bool part = false) {
   LeafArgs a;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
   a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
   a.P = pl.P; a.m = pl.m;
   a.out = out; a.ldo = ldo; a.out_block_stride = stride; a.alpha = alpha;
-  a.jobs = pl.d_jobs; a.n_jobs = pl.n_jobs;
+  a.jobs = part ? pl.d_jobs + pl.n_jobs : pl.d_jobs;
+  a.n_jobs = part ? pl.n_jobs_part : pl.n_jobs;
   a.rows = rows;
   MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
   return MF_OK;
@@ -273,8 +275,18 @@ const char* mf_last_error(void) { return g_err.c_str(); }
 
 const char* mf_version(void) { return "mf 0.1.0 sm_100a"; }
 
+static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double* U,
+                              const double* V, const double* W, int32_t levels, int64_t n,
+                              const mf_options* opt, bool allow_split);
+
 mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const double* V,
                   const double* W, int32_t levels, int64_t n, const mf_options* opt) {
+  return mf_plan_impl(out, p, R, U, V, W, levels, n, opt, true);
+}
+
+static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double* U,
+                              const double* V, const double* W, int32_t levels, int64_t n,
+                              const mf_options* opt, bool allow_split) {
   g_err.clear();
   if (!out) return fail(MF_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
@@ -317,7 +329,7 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     sub.shard_rank = 0; sub.shard_count = 1; sub.nccl_comm = nullptr; sub.profile = 0;
     sub.input_mode = MF_IN_REPLICATED;
     mf_plan_t parent = nullptr, child = nullptr;
-    mf_status st = mf_plan(&parent, p, R, U, V, W, 1, n, &top);
+    mf_status st = mf_plan_impl(&parent, p, R, U, V, W, 1, n, &top, false);
     if (st != MF_OK) return st;
     st = mf_plan(&child, p, R, U, V, W, levels - 1, n / p, &sub);
     if (st != MF_OK) {
@@ -368,11 +380,24 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
 
   // ---- classify operand columns: single +-1 entry => alias ----
   const int NB = pl->P * pl->P;
+  // Sharding: base = RL / N whole products per rank in contiguous
+  // ranges; the RL mod N leftovers are split by tile-aligned row slabs, rank r
+  // taking slab r of each (shard = -1).  Without enough tile rows, or for the
+  // parent of a level-by-level plan, the leftovers go whole to ranks instead.
+  const int64_t base = RL / shard_count, left = RL % shard_count;
+  const bool split = allow_split && levels > 0 && shard_count > 1 && left > 0 &&
+                     (pl->m + 127) / 128 >= shard_count;
+  if (split) {
+    const int64_t tiles = (pl->m + 127) / 128;
+    pl->part_r0 = std::min<int64_t>(pl->m, 128 * (pl->shard_rank * tiles / shard_count));
+    pl->part_r1 = std::min<int64_t>(pl->m, 128 * ((pl->shard_rank + 1) * tiles / shard_count));
+  }
   pl->prods.resize(RL);
   for (int64_t q = 0; q < RL; ++q) {
     Product& pr = pl->prods[q];
     pr.sign = 1;
-    pr.shard = (int32_t)((q * shard_count) / RL);
+    pr.shard = split ? (q < base * shard_count ? (int32_t)(q / base) : -1)
+                     : (int32_t)((q * shard_count) / RL);
     for (int side = 0; side < 2; ++side) {
       const std::vector<double>& M = side == 0 ? pl->U : pl->V;
       int nnz = 0, k0 = -1;
@@ -395,37 +420,51 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
   }
   pl->n_mat_a = (int)pl->mat_a_col.size();
   pl->n_mat_b = (int)pl->mat_b_col.size();
-  for (int64_t q = 0; q < RL; ++q)
+  for (int64_t q = 0; q < RL; ++q) {
     if (pl->prods[q].shard == pl->shard_rank) pl->my_prods.push_back((int32_t)q);
+    if (pl->prods[q].shard < 0) pl->my_part.push_back((int32_t)q);
+  }
 
   // unsharded plans of a compiled-in triple use the specialised K4/K6
   if (levels > 0 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) pl->fixed_id = fixed_match(*pl);
 
   // ---- mix tables for this shard ----
-  for (int side = 0; side < 2 && levels > 0; ++side) {
-    MixTable& t = side == 0 ? pl->mixA : pl->mixB;
+  auto add_slots = [&](MixTable& t, int side, const std::vector<int32_t>& qs) {
     const std::vector<double>& M = side == 0 ? pl->U : pl->V;
     t.nin = NB;
-    for (int32_t q : pl->my_prods) {
+    for (int32_t q : qs) {
       const Product& pr = pl->prods[q];
       if ((side == 0 ? pr.a_src : pr.b_src) != SRC_WORKSPACE) continue;
       for (int k = 0; k < NB; ++k) t.coef.push_back(M[k * RL + q]);
       t.out_map.push_back(side == 0 ? pr.a_idx : pr.b_idx);
       ++t.nout;
     }
-  }
-  if (levels > 0) {
-    MixTable& c = pl->mixC;
+  };
+  auto post_table = [&](MixTable& c, bool with_part) {
     c.nin = (int)RL;
     c.nout = NB;
     c.coef.assign((size_t)NB * RL, 0.0);
     for (int i = 0; i < NB; ++i) c.out_map.push_back(i);
     for (int32_t q : pl->my_prods)
       for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+    if (with_part)
+      for (int32_t q : pl->my_part)
+        for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+  };
+  if (levels > 0) {
+    std::vector<int32_t> all = pl->my_prods;
+    all.insert(all.end(), pl->my_part.begin(), pl->my_part.end());
+    std::sort(all.begin(), all.end());
+    add_slots(pl->mixA, 0, pl->my_prods);
+    add_slots(pl->mixA2, 0, pl->my_part);
+    add_slots(pl->mixB, 1, all);
+    post_table(pl->mixC, false);
+    if (!pl->my_part.empty()) post_table(pl->mixC2, true);
   }
 
   if (host_only) {  // host logic only: no device work, no workspace
     pl->n_jobs = (int)pl->my_prods.size();
+    pl->n_jobs_part = (int)pl->my_part.size();
     *out = pl.release();
     return MF_OK;
   }
@@ -441,13 +480,16 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     pl->ws_bytes = tb + sb + pb;
     mf_status st;
     if ((st = upload_table(pl->mixA)) != MF_OK || (st = upload_table(pl->mixB)) != MF_OK ||
-        (st = upload_table(pl->mixC)) != MF_OK) {
+        (st = upload_table(pl->mixC)) != MF_OK || (st = upload_table(pl->mixA2)) != MF_OK ||
+        (st = upload_table(pl->mixC2)) != MF_OK) {
       free_plan(pl.get());
       return st;
     }
   }
   std::vector<LeafJob> jobs;
-  for (int32_t q : pl->my_prods) {
+  std::vector<int32_t> job_q = pl->my_prods;
+  job_q.insert(job_q.end(), pl->my_part.begin(), pl->my_part.end());
+  for (int32_t q : job_q) {
     const Product& pr = pl->prods[q];
     LeafJob j;
     j.a_coord = pr.a_src == SRC_INPUT ? ((pr.a_idx / pl->P) << 16) | (pr.a_idx % pl->P) : pr.a_idx;
@@ -456,7 +498,8 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
     j.out_idx = levels > 0 ? q : 0;
     jobs.push_back(j);
   }
-  pl->n_jobs = (int)jobs.size();
+  pl->n_jobs = (int)pl->my_prods.size();
+  pl->n_jobs_part = (int)pl->my_part.size();
   if (!jobs.empty()) {
     if (cudaMalloc(&pl->d_jobs, sizeof(LeafJob) * jobs.size()) != cudaSuccess) {
       free_plan(pl.get());
@@ -489,6 +532,13 @@ mf_status mf_plan_info(mf_plan_t pl, size_t* ws, int64_t* leaf_n, int64_t* n_pro
   if (n_products) *n_products = pl->RL;
   if (n_mat_a) *n_mat_a = pl->n_mat_a;
   if (n_mat_b) *n_mat_b = pl->n_mat_b;
+  return MF_OK;
+}
+
+mf_status mf_plan_shard_rows(mf_plan_t pl, int64_t* r0, int64_t* r1) {
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (r0) *r0 = pl->my_part.empty() ? 0 : pl->part_r0;
+  if (r1) *r1 = pl->my_part.empty() ? 0 : pl->part_r1;
   return MF_OK;
 }
 
@@ -566,6 +616,11 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
     MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
+    if (!pl->my_part.empty()) {
+      Rows pr;
+      pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
+      MF_CUDA(launch_premix(*pl, pl->mixA2, A, lda, pl->T, s, pr), "pre-add A (K4, split)");
+    }
     mark(1);
     MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
     mark(2);
@@ -588,14 +643,31 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
           return st;
       }
     } else {
-      // a3: all leaf products in one launch (K5)
+      // a3: all leaf products in one launch (K5); split products on this rank's slab
       if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) !=
           MF_OK)
         return st;
+      if (!pl->my_part.empty()) {
+        Rows pr;
+        pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
+        if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s, pr,
+                           true)) != MF_OK)
+          return st;
+      }
     }
     mark(3);
-    // a4: fused post-addition (K6)
-    MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
+    // a4: fused post-addition (K6); rows holding split-product slabs use mixC2
+    if (pl->my_part.empty()) {
+      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
+    } else {
+      Rows lo, mid, hi;
+      lo.r1 = pl->part_r0;
+      mid.r0 = pl->part_r0; mid.r1 = pl->part_r1;
+      hi.r0 = pl->part_r1;
+      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, C, ldc, s, lo), "post-add (K6)");
+      MF_CUDA(launch_postmix(*pl, pl->mixC2, alpha, pl->Pw, C, ldc, s, mid), "post-add (K6)");
+      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, C, ldc, s, hi), "post-add (K6)");
+    }
   }
   mark(4);
   if (pl->nccl_comm) {
@@ -723,7 +795,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     } else {
       if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, rg)) != MF_OK)
         return st;
-      MF_CUDA(launch_postmix(*pl, alpha, pl->Pw, dC, n, s, rg), "post-add (K6)");
+      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, dC, n, s, rg), "post-add (K6)");
     }
     cudaEvent_t ev = e_c[next_c++];
     MF_CUDA(cudaEventRecord(ev, s), "event");
@@ -821,7 +893,8 @@ mf_status mf_postmix(mf_plan_t pl, double alpha, const double* P, double* C, int
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no post-addition");
   DeviceGuard guard(pl->device);
-  MF_CUDA(launch_postmix(*pl, alpha, P, C, ldc, static_cast<cudaStream_t>(stream)), "post-add (K6)");
+  MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, P, C, ldc, static_cast<cudaStream_t>(stream)),
+          "post-add (K6)");
   return MF_OK;
 }
 

@@ -75,10 +75,17 @@ struct Plan {
   int leaf = MF_LEAF_DMMA;
   int fixed_id = 0;  // > 0: compile-time specialised K4/K6 (mf_fixed.cu) for this triple
   int shard_rank = 0, shard_count = 1;
-  // shard-local view: the products this plan's rank computes
-  std::vector<int32_t> my_prods;  // product indices q
-  MixTable mixA, mixB;            // pre-additions for the slots my_prods use
-  MixTable mixC;                  // post-addition over ALL products (zero coef outside shard)
+  // shard-local view: the products this plan's rank computes whole,
+  // and the leftover products (R^L mod N of them) of which every rank computes
+  // the row slab part_rows -- exact balance at R^L / N products per rank
+  std::vector<int32_t> my_prods;  // whole products q
+  std::vector<int32_t> my_part;   // split products q (this rank: rows part_rows)
+  int64_t part_r0 = 0, part_r1 = 0;
+  MixTable mixA, mixB;            // pre-additions: A slots of whole products, all B slots used
+  MixTable mixA2;                 // A slots of split products (rows part_rows only)
+  MixTable mixC;                  // post-addition over the whole products (zero coef elsewhere)
+  MixTable mixC2;                 // ... plus the split products (used on rows part_rows)
+  int n_jobs_part = 0;            // leaf jobs of split products follow the whole ones in d_jobs
   // device memory
   double* T = nullptr;   // n_mat_a x m x m
   double* S = nullptr;   // n_mat_b x m x m
@@ -115,8 +122,8 @@ struct Rows {
 // ---- launchers (mf_mix.cu, mf_leaf.cu); return cudaError_t of the launch ----
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows = Rows());
-cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C,
-                           int64_t ldc, cudaStream_t s, Rows rows = Rows());
+cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
+                           double* C, int64_t ldc, cudaStream_t s, Rows rows = Rows());
 
 struct LeafArgs {
   // operand views: matrices (4-D block view, SRC_INPUT) and workspaces (3-D)

@@ -213,13 +213,13 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
                       1.0, s, rows);
 }
 
-cudaError_t launch_postmix(const Plan& pl, double alpha, const double* Pw, double* C, int64_t ldc,
-                           cudaStream_t s, Rows rows) {
+cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
+                           double* C, int64_t ldc, cudaStream_t s, Rows rows) {
   if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
+  if (pl.fixed_id > 0 && &t == &pl.mixC && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
     return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
-  return mix_dispatch(vw, pl.mixC, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
+  return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
                       pl.m, alpha, s, rows);
 }
 

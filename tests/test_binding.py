@@ -134,3 +134,22 @@ def test_host_only_sharding_balanced():
     counts = np.bincount(sh, minlength=8)
     assert counts.sum() == 49 and counts.max() - counts.min() <= 1
     assert (np.diff(sh) >= 0).all()  # contiguous ranges
+
+
+@pytest.mark.parametrize("N", [2, 3, 5, 8])
+def test_host_only_split_sharding_exact_balance(N):
+    """49 products on N ranks = floor(49/N) whole products each plus a
+    row slab of every leftover product; the slabs tile [0, m) exactly once."""
+    n = 4096
+    m = n // 4
+    slabs, whole = [], []
+    for r in range(N):
+        p = mf.Plan(triples.STRASSEN_WINOGRAD, 2, n, shard_rank=r, shard_count=N, host_only=True)
+        sh = p.products()["shard"]
+        whole.append(int((sh == r).sum()))
+        assert int((sh == -1).sum()) == 49 % N
+        slabs.append(p.shard_rows())
+    assert whole == [49 // N] * N
+    assert slabs[0][0] == 0 and slabs[-1][1] == m
+    assert all(slabs[i][1] == slabs[i + 1][0] for i in range(N - 1))
+    assert all(a % 128 == 0 for a, _ in slabs)

@@ -269,6 +269,31 @@ def test_sharded_partials_sum_to_product():
     assert (owners[0] == owners[1]).all() and sorted(set(owners[0].tolist())) == [0, 1, 2]
 
 
+@pytest.mark.parametrize("N", [2, 3, 8])
+def test_split_sharding_partials_sum_to_product(N):
+    """Exact balance emulated on one GPU: floor(49/N) whole products
+    per rank + a row slab of each leftover product; the N partial C sum to the
+    exact product on integers, and to the 1-GPU result within the bound."""
+    n = 4096
+    A, B = mf_inputs.pair("int1024", n, 19)
+    Ad, Bd = dev(A), dev(B)
+    total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N) as p:
+            assert (p.products()["shard"] == -1).sum() == 49 % N
+            total += p.dgemm(Ad, Bd)
+    assert (host(total) == exact(A, B)).all()
+    A, B = mf_inputs.pair("uniform", n, 20)
+    Ad, Bd = dev(A), dev(B)
+    with mf.Plan(triples.get(SW), 2, n) as p:
+        ref = host(p.dgemm(Ad, Bd))
+    total.zero_()
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N) as p:
+            total += p.dgemm(Ad, Bd)
+    assert scaled(host(total), ref, A, B) <= 2e-13
+
+
 def run_plan(p, A, B):
     return host(p.dgemm(dev(A), dev(B)))
 
