@@ -229,8 +229,8 @@ void free_plan(Plan* pl) {
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
-  if (pl->h2d) cudaStreamDestroy(pl->h2d);
-  if (pl->d2h) cudaStreamDestroy(pl->d2h);
+  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
+    if (st) cudaStreamDestroy(st);
 }
 
 // Events of the current call when profiling is on (nullptr otherwise).
@@ -705,17 +705,19 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
   return MF_OK;
 }
 
-// Host-buffer pipeline.  The leaf of output rows r needs A's
-// row slab r (of every block) and all of B; its columns c need only B's
-// column slab c.  Schedule (copy stream h2d, the call's stream s, copy stream
-// d2h):
-//   h2d: A slabs 0..H-1, then B column slabs 0..NC-1, then A slabs H..NS-1;
-//   s:   for each column slab c: K4(B) on it, then for the first H row slabs
-//        K4(A) (once), K5 and K6 on region (r, c); then row slabs H..NS-1
-//        whole: K4(A), K5, K6;
-//   d2h: each finished C region, as soon as it is done.
-// Compute starts after ~(H/NS + 1/NC) of the inputs crossed PCIe and the
-// remaining copies overlap compute; results are bitwise those of mf_dgemm.
+// Host-buffer pipeline.  Output region (i, j) -- rows of slab
+// i, columns of slab j of every block -- needs A's row slab i and B's column
+// slab j only (K4(A) on rows i, K4(B) on columns j, then K5 and K6 on the
+// region).  Schedule:
+//   h2d  : A_0, B_0, A_1, B_1, ... (interleaved, 1/NS and 1/NC of each)
+//   mixs : (high priority) K4(A_i) / K4(B_j) as soon as the slab has landed
+//   s, s2: regions in "shells" k = max(i, j) -- (k,0..k-1) then (0..k, k) --
+//          alternating between two streams so one region's last wave overlaps
+//          the next region's first
+//   d2h  : each finished C region
+// Compute starts after 1/NS + 1/NC of an input crossed PCIe; everything else
+// overlaps.  Results are bitwise those of mf_dgemm (same kernels, same order
+// per element).
 static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child) return 1;
   const int64_t tiles = (pl.m + 127) / 128;
@@ -759,106 +761,117 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   }
   const int64_t m = pl->m;
   const int P = pl->P;
-  const int nc = (int)std::min<int64_t>(4, (m + 127) / 128);  // B column slabs
-  const int head = std::min(2, ns);                            // row slabs done column-wise
+  const int nc = ns;  // square grid of regions
   if (!pl->h2d) MF_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking), "stream");
   if (!pl->d2h) MF_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking), "stream");
-  const size_t nev = 3 + ns + nc + (size_t)head * nc + ns;
+  if (!pl->s2) MF_CUDA(cudaStreamCreateWithFlags(&pl->s2, cudaStreamNonBlocking), "stream");
+  if (!pl->mixs) {
+    int lo = 0, hi = 0;
+    MF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    MF_CUDA(cudaStreamCreateWithPriority(&pl->mixs, cudaStreamNonBlocking, hi), "stream");
+  }
+  const size_t nev = 4 + 2 * (size_t)ns + 2 * (size_t)nc + (size_t)ns * nc;
   while (pl->pipe_events.size() < nev) {
     cudaEvent_t e;
     MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     pl->pipe_events.push_back(e);
   }
-  cudaEvent_t e_start = pl->pipe_events[0], e_done = pl->pipe_events[1];
-  cudaEvent_t* e_a = &pl->pipe_events[3];
-  cudaEvent_t* e_b = e_a + ns;
-  cudaEvent_t* e_c = e_b + nc;
-  int next_c = 0;
+  cudaEvent_t e_start = pl->pipe_events[0], e_done = pl->pipe_events[1], e_s2 = pl->pipe_events[2];
+  cudaEvent_t* e_a = &pl->pipe_events[4];   // A slab i landed
+  cudaEvent_t* e_b = e_a + ns;              // B slab j landed
+  cudaEvent_t* e_pa = e_b + nc;             // K4(A_i) done
+  cudaEvent_t* e_pb = e_pa + ns;            // K4(B_j) done
+  cudaEvent_t* e_c = e_pb + nc;             // region done
   const double* dA = pl->hA;
   const double* dB = pl->hB;
   double* dC = pl->hC;
+  int region_no = 0;
 
-  auto h2d_a_slab = [&](int r) -> mf_status {
-    const auto sr = tile_piece(m, r, ns);
-    for (int br = 0; br < P; ++br) {
-      const int64_t row = br * m + sr.first;
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
-                                sr.second - sr.first, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
+  MF_CUDA(cudaEventRecord(e_start, s), "event");
+  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
+    MF_CUDA(cudaStreamWaitEvent(st, e_start, 0), "wait");
+  // h2d: A_0, B_0, A_1, B_1, ...
+  for (int k = 0; k < std::max(ns, nc); ++k) {
+    if (k < ns) {
+      const auto sr = tile_piece(m, k, ns);
+      for (int br = 0; br < P; ++br) {
+        const int64_t row = br * m + sr.first;
+        MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
+                                  sr.second - sr.first, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
+      }
+      MF_CUDA(cudaEventRecord(e_a[k], pl->h2d), "event");
     }
-    MF_CUDA(cudaEventRecord(e_a[r], pl->h2d), "event");
-    return MF_OK;
-  };
-  // compute + D2H of one region of every C block
-  auto region = [&](Rows rg) -> mf_status {
+    if (k < nc) {
+      const auto sc = tile_piece(m, k, nc);
+      for (int bc = 0; bc < P; ++bc)
+        MF_CUDA(cudaMemcpy2DAsync(pl->hB + bc * m + sc.first, n * 8, B + bc * m + sc.first, ldb * 8,
+                                  (sc.second - sc.first) * 8, n, cudaMemcpyHostToDevice, pl->h2d),
+                "H2D B slab");
+      MF_CUDA(cudaEventRecord(e_b[k], pl->h2d), "event");
+    }
+  }
+  // mixs: K4 per slab, as soon as it landed
+  for (int k = 0; k < std::max(ns, nc); ++k) {
+    if (k < ns) {
+      MF_CUDA(cudaStreamWaitEvent(pl->mixs, e_a[k], 0), "wait");
+      const auto sr = tile_piece(m, k, ns);
+      Rows rows;
+      rows.r0 = sr.first; rows.r1 = sr.second;
+      if (pl->levels > 0)
+        MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, pl->mixs, rows), "pre-add A (K4)");
+      MF_CUDA(cudaEventRecord(e_pa[k], pl->mixs), "event");
+    }
+    if (k < nc) {
+      MF_CUDA(cudaStreamWaitEvent(pl->mixs, e_b[k], 0), "wait");
+      const auto sc = tile_piece(m, k, nc);
+      Rows cols;
+      cols.c0 = sc.first; cols.c1 = sc.second;
+      if (pl->levels > 0)
+        MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, pl->mixs, cols), "pre-add B (K4)");
+      MF_CUDA(cudaEventRecord(e_pb[k], pl->mixs), "event");
+    }
+  }
+  // regions in shells, alternating compute streams
+  auto region = [&](int i, int j) -> mf_status {
+    cudaStream_t cs = (region_no & 1) ? pl->s2 : s;
+    MF_CUDA(cudaStreamWaitEvent(cs, e_pa[i], 0), "wait");
+    MF_CUDA(cudaStreamWaitEvent(cs, e_pb[j], 0), "wait");
+    const auto sr = tile_piece(m, i, ns);
+    const auto sc = tile_piece(m, j, nc);
+    Rows rg;
+    rg.r0 = sr.first; rg.r1 = sr.second; rg.c0 = sc.first; rg.c1 = sc.second;
     if (pl->levels == 0) {
-      if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, s, rg)) != MF_OK) return st;
+      if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, cs, rg)) != MF_OK) return st;
     } else {
-      if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, rg)) != MF_OK)
+      if ((st = run_leaf(*pl, dA, n, dB, n, pl->T, pl->S, pl->Pw, m, m * m, 1.0, cs, rg)) != MF_OK)
         return st;
-      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, dC, n, s, rg), "post-add (K6)");
+      MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, dC, n, cs, rg), "post-add (K6)");
     }
-    cudaEvent_t ev = e_c[next_c++];
-    MF_CUDA(cudaEventRecord(ev, s), "event");
+    cudaEvent_t ev = e_c[region_no++];
+    MF_CUDA(cudaEventRecord(ev, cs), "event");
     MF_CUDA(cudaStreamWaitEvent(pl->d2h, ev, 0), "wait");
-    const int64_t r0 = rg.r0, r1 = rg.end(m), c0 = rg.c0, c1 = rg.cend(m);
     for (int br = 0; br < P; ++br)
       for (int bc = 0; bc < P; ++bc) {
-        const int64_t off = bc * m + c0;  // column offset of block (br, bc)'s region
-        MF_CUDA(cudaMemcpy2DAsync(C + (br * m + r0) * ldc + off, ldc * 8, dC + (br * m + r0) * n + off,
-                                  n * 8, (c1 - c0) * 8, r1 - r0, cudaMemcpyDeviceToHost, pl->d2h),
+        const int64_t row = br * m + rg.r0, col = bc * m + rg.c0;
+        MF_CUDA(cudaMemcpy2DAsync(C + row * ldc + col, ldc * 8, dC + row * n + col, n * 8,
+                                  (rg.c1 - rg.c0) * 8, rg.r1 - rg.r0, cudaMemcpyDeviceToHost,
+                                  pl->d2h),
                 "D2H C region");
       }
     return MF_OK;
   };
-
-  // prior work on the call's stream (which may still read the plan buffers) first
-  MF_CUDA(cudaEventRecord(e_start, s), "event");
-  MF_CUDA(cudaStreamWaitEvent(pl->h2d, e_start, 0), "wait");
-  MF_CUDA(cudaStreamWaitEvent(pl->d2h, e_start, 0), "wait");
-  for (int r = 0; r < head; ++r)
-    if ((st = h2d_a_slab(r)) != MF_OK) return st;
-  for (int c = 0; c < nc; ++c) {
-    const auto sc = tile_piece(m, c, nc);
-    for (int bc = 0; bc < P; ++bc)
-      MF_CUDA(cudaMemcpy2DAsync(pl->hB + bc * m + sc.first, n * 8, B + bc * m + sc.first, ldb * 8,
-                                (sc.second - sc.first) * 8, n, cudaMemcpyHostToDevice, pl->h2d),
-              "H2D B column slab");
-    MF_CUDA(cudaEventRecord(e_b[c], pl->h2d), "event");
-  }
-  for (int r = head; r < ns; ++r)
-    if ((st = h2d_a_slab(r)) != MF_OK) return st;
-
-  for (int c = 0; c < nc; ++c) {
-    const auto sc = tile_piece(m, c, nc);
-    MF_CUDA(cudaStreamWaitEvent(s, e_b[c], 0), "wait");
-    if (pl->levels > 0) {
-      Rows cols;
-      cols.c0 = sc.first; cols.c1 = sc.second;
-      MF_CUDA(launch_premix(*pl, pl->mixB, dB, n, pl->S, s, cols), "pre-add B (K4)");
-    }
-    for (int r = 0; r < head; ++r) {
-      const auto sr = tile_piece(m, r, ns);
-      if (c == 0) {
-        MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
-        Rows rows;
-        rows.r0 = sr.first; rows.r1 = sr.second;
-        if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
-      }
-      Rows rg;
-      rg.r0 = sr.first; rg.r1 = sr.second; rg.c0 = sc.first; rg.c1 = sc.second;
-      if ((st = region(rg)) != MF_OK) return st;
-    }
-  }
-  for (int r = head; r < ns; ++r) {
-    const auto sr = tile_piece(m, r, ns);
-    MF_CUDA(cudaStreamWaitEvent(s, e_a[r], 0), "wait");
-    Rows rows;
-    rows.r0 = sr.first; rows.r1 = sr.second;
-    if (pl->levels > 0) MF_CUDA(launch_premix(*pl, pl->mixA, dA, n, pl->T, s, rows), "pre-add A (K4)");
-    if ((st = region(rows)) != MF_OK) return st;
+  for (int k = 0; k < std::max(ns, nc); ++k) {
+    if (k < ns)
+      for (int j = 0; j < std::min(k, nc); ++j)
+        if ((st = region(k, j)) != MF_OK) return st;
+    if (k < nc)
+      for (int i = 0; i <= std::min(k, ns - 1); ++i)
+        if ((st = region(i, k)) != MF_OK) return st;
   }
   MF_CUDA(cudaEventRecord(e_done, pl->d2h), "event");
-  MF_CUDA(cudaStreamWaitEvent(s, e_done, 0), "wait");  // keep the call's stream ordered after D2H
+  MF_CUDA(cudaEventRecord(e_s2, pl->s2), "event");
+  MF_CUDA(cudaStreamWaitEvent(s, e_s2, 0), "wait");    // the call's stream ends after all work
+  MF_CUDA(cudaStreamWaitEvent(s, e_done, 0), "wait");
   MF_CUDA(cudaEventSynchronize(e_done), "cudaEventSynchronize");
   return MF_OK;
 }

@@ -102,7 +102,7 @@ struct Plan {
   // leaf product (levels - 1 levels at n / p); this plan is then one level
   Plan* child = nullptr;
   // host-buffer pipeline (mf_dgemm_host): copy streams and per-slab events
-  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr, mixs = nullptr, s2 = nullptr;
   std::vector<cudaEvent_t> pipe_events;
   // phase profiling (mf_options.profile): 6 events per mf_dgemm call
   std::vector<std::vector<cudaEvent_t>> prof_events;
