@@ -426,7 +426,10 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   }
 
   // unsharded plans of a compiled-in triple use the specialised K4/K6
-  if (levels > 0 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) pl->fixed_id = fixed_match(*pl);
+  if (levels > 0 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) {
+    pl->fixed_id = fixed_match(*pl);
+    if (pl->fixed_id == 0) pl->fixed_id = kron_match(*pl);
+  }
 
   // ---- mix tables for this shard ----
   auto add_slots = [&](MixTable& t, int side, const std::vector<int32_t>& qs) {

@@ -17,76 +17,10 @@
 #include <utility>
 
 #include "mf_internal.h"
+#include "mf_tables.h"
 
 namespace mf {
 namespace fixed {
-
-template <int NB, int R>
-struct Tri {
-  int8_t U[NB][R], V[NB][R], W[NB][R];
-};
-
-// Blocks 0=(1,1) 1=(1,2) 2=(2,1) 3=(2,2); W rows in natural C order.
-inline constexpr Tri<4, 7> kSW = {
-    {{1, 0, 1, 0, 0, -1, 1}, {0, 1, 1, 0, 0, 0, 0}, {0, 0, -1, 0, 1, 1, -1}, {0, 0, -1, 1, 1, 1, 0}},
-    {{1, 0, 0, 1, -1, 1, 0}, {0, 0, 0, -1, 1, -1, -1}, {0, 1, 0, -1, 0, 0, 0}, {0, 0, 1, 1, 0, 1, 1}},
-    {{1, 1, 0, 0, 0, 0, 0}, {1, 0, 1, 0, 1, 1, 0}, {1, 0, 0, -1, 0, 1, 1}, {1, 0, 0, 0, 1, 1, 1}}};
-inline constexpr Tri<4, 7> kPS = {
-    {{0, 1, 1, 0, 1, 1, 0}, {0, 0, -1, 1, 0, 0, 0}, {1, 1, 1, 0, 1, 0, 0}, {-1, -1, -1, 0, 0, 0, 1}},
-    {{0, 0, 0, 0, 1, 1, 0}, {1, 1, 0, 0, 1, 0, 1}, {0, 1, 1, 1, 1, 0, 0}, {0, 1, 1, 0, 1, 0, 1}},
-    {{0, 0, 0, 1, 0, 1, 0}, {-1, 1, -1, -1, 0, 0, 0}, {0, -1, 0, 0, 1, -1, -1}, {1, 0, 0, 0, 0, 0, 1}}};
-inline constexpr Tri<4, 7> kS69 = {
-    {{1, 0, 1, 0, 1, -1, 0}, {0, 0, 0, 0, 1, 0, 1}, {0, 1, 0, 0, 0, 1, 0}, {1, 1, 0, 1, 0, 0, -1}},
-    {{1, 1, 0, -1, 0, 1, 0}, {0, 0, 1, 0, 0, 1, 0}, {0, 0, 0, 1, 0, 0, 1}, {1, 0, -1, 0, 1, 0, 1}},
-    {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0}, {0, 1, 0, 1, 0, 0, 0}, {1, -1, 1, 0, 0, 1, 0}}};
-// Laderman 1976, blocks 0..8 row-major over the 3x3 grid.
-inline constexpr Tri<9, 23> kLD = {
-    {{1, 1, 0, -1, 0, 1, -1, -1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-     {1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
-     {1, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, -1, 1, 1, 0, -1, 1, 0, 0, 0, 0, 0, 0},
-     {-1, -1, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0},
-     {-1, 0, 1, 1, 1, 0, 0, 0, 0, -1, 0, 0, 0, 0, 0, 1, 0, 1, 0, 0, 0, 0, 0},
-     {0, 0, 0, 0, 0, 0, 0, 0, 0, -1, 0, 0, 0, 0, 0, 1, -1, 1, 0, 1, 0, 0, 0},
-     {0, 0, 0, 0, 0, 0, 1, 1, 1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},
-     {-1, 0, 0, 0, 0, 0, 1, 0, 1, -1, 1, 1, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0},
-     {-1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, -1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1}},
-    {{0, 0, -1, 1, -1, 1, 1, 0, -1, 0, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-     {0, -1, 1, -1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0},
-     {0, 0, 0, 0, 0, 0, -1, 1, 1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0},
-     {0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
-     {1, 1, -1, 1, 0, 0, 0, 0, 0, 0, -1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-     {0, 0, -1, 0, 0, 0, 1, -1, 0, 1, -1, 0, 0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0},
-     {0, 0, -1, 0, 0, 0, 0, 0, 0, 0, -1, 1, 0, 1, -1, 1, 0, -1, 0, 0, 0, 0, 0},
-     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, -1, -1, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0},
-     {0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, -1, -1, 1, 0, 0, 0, 0, 1}},
-    {{0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0},
-     {1, 0, 0, 1, 1, 1, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0},
-     {0, 0, 0, 0, 0, 1, 1, 0, 1, 1, 0, 0, 0, 1, 0, 1, 0, 1, 0, 0, 0, 0, 0},
-     {0, 1, 1, 1, 0, 1, 0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 0, 0, 0, 0},
-     {0, 1, 0, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0},
-     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 1, 0, 0, 1, 0, 0},
-     {0, 0, 0, 0, 0, 1, 1, 1, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 1, 0},
-     {0, 0, 0, 0, 0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1}}};
-
-// PAPER.md L303-309 with SPEC.md L244's row interleave; q = qo*Ri + qi.
-template <int Po, int NBo, int Ro, int Pi, int NBi, int Ri>
-constexpr Tri<NBo * NBi, Ro * Ri> kron(const Tri<NBo, Ro>& o, const Tri<NBi, Ri>& in) {
-  Tri<NBo * NBi, Ro * Ri> t{};
-  constexpr int P = Po * Pi;
-  for (int b = 0; b < NBo; ++b)
-    for (int s = 0; s < NBi; ++s) {
-      const int row = ((b / Po) * Pi + s / Pi) * P + (b % Po) * Pi + s % Pi;
-      for (int qo = 0; qo < Ro; ++qo)
-        for (int qi = 0; qi < Ri; ++qi) {
-          const int q = qo * Ri + qi;
-          t.U[row][q] = (int8_t)(o.U[b][qo] * in.U[s][qi]);
-          t.V[row][q] = (int8_t)(o.V[b][qo] * in.V[s][qi]);
-          t.W[row][q] = (int8_t)(o.W[b][qo] * in.W[s][qi]);
-        }
-    }
-  return t;
-}
 
 inline constexpr Tri<16, 49> kSW2 = kron<2, 4, 7, 2, 4, 7>(kSW, kSW);
 inline constexpr Tri<16, 49> kPS2 = kron<2, 4, 7, 2, 4, 7>(kPS, kPS);
@@ -94,10 +28,6 @@ inline constexpr Tri<16, 49> kS692 = kron<2, 4, 7, 2, 4, 7>(kS69, kS69);
 
 // Kernel templates are parameterised by a tag TYPE (nvcc's host stubs cannot
 // name reference template arguments); device helpers take the reference.
-struct TagSW { static constexpr const auto& T = kSW; };
-struct TagPS { static constexpr const auto& T = kPS; };
-struct TagS69 { static constexpr const auto& T = kS69; };
-struct TagLD { static constexpr const auto& T = kLD; };
 struct TagSW2 { static constexpr const auto& T = kSW2; };
 struct TagPS2 { static constexpr const auto& T = kPS2; };
 struct TagS692 { static constexpr const auto& T = kS692; };

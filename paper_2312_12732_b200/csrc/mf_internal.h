@@ -73,7 +73,7 @@ struct Plan {
   std::vector<int32_t> mat_a_col, mat_b_col;  // slot -> product column q
   mf_options opt{};
   int leaf = MF_LEAF_DMMA;
-  int fixed_id = 0;  // > 0: compile-time specialised K4/K6 (mf_fixed.cu) for this triple
+  int fixed_id = 0;  // 1..7: flattened K4/K6 (mf_fixed.cu); 8..: Kronecker-factored (mf_kron.cu)
   int shard_rank = 0, shard_count = 1;
   // shard-local view: the products this plan's rank computes whole,
   // and the leftover products (R^L mod N of them) of which every rank computes
@@ -149,6 +149,12 @@ cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, 
                                 double* out, cudaStream_t s, Rows rows);
 cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
                                  int64_t ldc, cudaStream_t s, Rows rows);
+// mf_kron.cu: Kronecker-factored K4/K6 for deep powers (ids >= 8)
+int kron_match(const Plan& pl);
+cudaError_t launch_premix_kron(int id, int side, const double* X, int64_t ldx, int64_t m,
+                               double* out, cudaStream_t s, Rows rows);
+cudaError_t launch_postmix_kron(int id, const double* Pw, int64_t m, double alpha, double* C,
+                                int64_t ldc, cudaStream_t s, Rows rows);
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s);
 
 }  // namespace mf

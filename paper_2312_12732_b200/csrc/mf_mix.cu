@@ -206,6 +206,8 @@ static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, in
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows) {
   if (t.nrow == 0 || rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
+  if (pl.fixed_id >= 8)
+    return launch_premix_kron(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s, rows);
   if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
     return launch_premix_fixed(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s, rows);
   const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
@@ -216,7 +218,9 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
 cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
                            double* C, int64_t ldc, cudaStream_t s, Rows rows) {
   if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  if (pl.fixed_id > 0 && &t == &pl.mixC && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
+  if (pl.fixed_id >= 8 && &t == &pl.mixC)
+    return launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
+  if (pl.fixed_id > 0 && pl.fixed_id < 8 && &t == &pl.mixC && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
     return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
   return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},

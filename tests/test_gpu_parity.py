@@ -101,6 +101,14 @@ def _flat_oracle_triple(name, levels):
     return oracle.kron_power(oracle.catalog(name), levels)
 
 
+def _kron_factored(name, levels, path):
+    """True when the plan runs the Kronecker-factored K4/K6 (mf_kron.cu), whose
+    order is the recursion's (tested against it below), not the flat table's."""
+    deep = (levels >= 3 and name in (SW, "paper-strassen", "strassen-1969")) or \
+        (levels == 2 and name == "laderman")
+    return path == "fixed" and deep
+
+
 MIX_PATHS = ["fixed", "generic"]  # compile-time specialised K4/K6 vs table-driven kernels
 
 
@@ -118,6 +126,8 @@ def _mix_path(monkeypatch, path):
                                            ("strassen-1969", 2, 64), (SW, 3, 128)])
 def test_premix_bit_exact(name, levels, n, path, monkeypatch):
     _mix_path(monkeypatch, path)
+    if _kron_factored(name, levels, path):
+        pytest.skip("Kronecker-factored path: see test_kron_factored_mix_bit_exact_with_recursion")
     A, B = mf_inputs.pair("uniform", n, 5)
     to = _flat_oracle_triple(name, levels)
     with mf.Plan(triples.get(name), levels, n) as p:
@@ -141,6 +151,8 @@ def test_premix_bit_exact(name, levels, n, path, monkeypatch):
                                            ("strassen-1969", 1, 64), (SW, 3, 128)])
 def test_postmix_bit_exact(name, levels, n, path, monkeypatch):
     _mix_path(monkeypatch, path)
+    if _kron_factored(name, levels, path):
+        pytest.skip("Kronecker-factored path: see test_kron_factored_mix_bit_exact_with_recursion")
     to = _flat_oracle_triple(name, levels)
     m = n // to.p
     rng = np.random.Generator(np.random.PCG64(9))
@@ -152,6 +164,56 @@ def test_postmix_bit_exact(name, levels, n, path, monkeypatch):
             p.postmix(dev(Pp), C, alpha=alpha)
             ref = oracle.postmix(Pp * sign[:, None, None], to, n, alpha)
             assert (host(C) == ref).all()
+
+
+def _recursive_premix(X, t, levels, side):
+    """The oracle's recursion (or_fmm) for the operands: level-1
+    T_q of X, then level-2 T of each, ... -> R^levels blocks, index outer-major."""
+    blocks = [X]
+    for _ in range(levels):
+        blocks = [T for Y in blocks for T in oracle.premix(Y, t, side)]
+    return np.stack(blocks)
+
+
+def _recursive_postmix(P, t, levels, n, alpha):
+    """The oracle's recursion for the post-addition: combine the innermost level
+    first ("recursively solve P_i and distribute it"), alpha last."""
+    cur = list(P)
+    size = n // t.p ** levels
+    for lev in range(levels):
+        size *= t.p
+        a = alpha if lev == levels - 1 else 1.0
+        cur = [oracle.postmix(np.stack(cur[g * t.R:(g + 1) * t.R]), t, size, a)
+               for g in range(len(cur) // t.R)]
+    return cur[0]
+
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 3, 128), ("paper-strassen", 3, 64),
+                                           ("strassen-1969", 3, 64), ("laderman", 2, 144),
+                                           (SW, 3, 200)])
+def test_kron_factored_mix_bit_exact_with_recursion(name, levels, n):
+    """Kronecker-factored K4/K6 (mf_kron.cu) == the oracle's recursive
+    pre-/post-additions bitwise on random fp64 (same per-level order)."""
+    t = triples.get(name)
+    to = oracle.catalog(name)
+    A, B = mf_inputs.pair("uniform", n, 23)
+    with mf.Plan(t, levels, n) as p:
+        info, pr = p.info(), p.products()
+        m = info["leaf_n"]
+        for side, X, src, idx in (("A", A, pr["a_src"], pr["a_idx"]), ("B", B, pr["b_src"], pr["b_idx"])):
+            nmat = info["n_mat_a"] if side == "A" else info["n_mat_b"]
+            out = torch.empty((nmat, m, m), dtype=torch.float64, device="cuda")
+            p.premix(side, dev(X), out)
+            got = host(out)
+            ref = _recursive_premix(X, to, levels, side)
+            for q in np.nonzero(src == 1)[0]:
+                assert (got[idx[q]] == ref[q]).all(), (side, q)
+        rng = np.random.Generator(np.random.PCG64(24))
+        Pp = rng.uniform(-1, 1, size=(to.R ** levels, m, m))
+        for alpha in (1.0, -1.25):
+            C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            p.postmix(dev(Pp), C, alpha=alpha)
+            assert (host(C) == _recursive_postmix(Pp, to, levels, n, alpha)).all()
 
 
 def test_leaf_stage_matches_oracle_products_on_integers():
