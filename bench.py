@@ -51,6 +51,10 @@ CONFIGS = {
     "c4a-ld1-13824": (13824, "laderman", 1),
     "c4b-sw2-13824": (13824, "strassen-winograd", 2),     # <4,4,4;49> = SW (x) SW
     "c5-sw2-32768": (32768, "strassen-winograd", 2),      # config 5's problem (1-GPU leg)
+    # deeper flattening at the same sizes (beyond the configs' level counts)
+    "x-sw3-16384": (16384, "strassen-winograd", 3),
+    "x-ld2-13824": (13824, "laderman", 2),
+    "x-sw3-32768": (32768, "strassen-winograd", 3),
 }
 
 
@@ -70,6 +74,8 @@ def parse():
     ap.add_argument("--no-classical", action="store_true")
     ap.add_argument("--level-by-level", action="store_true",
                     help="ablation: the paper's recursion instead of the flattened triple")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip timing the deeper-flattening variant (same n, one more level)")
     a = ap.parse_args()
     if a.config:
         a.n, a.triple, a.levels = CONFIGS[a.config]
@@ -342,6 +348,32 @@ def main():
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
                       "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step)"}
         out["gpu_launches_e2e_per_step"] = 4 if a.levels > 0 else 1
+
+    # ---- the same n with one more recursion level (deeper flattening), same run ----
+    if rank == 0 and world == 1 and not a.no_variants and a.triple == "strassen-winograd" \
+            and a.levels == 2 and not a.level_by_level and a.n % 8 == 0:
+        torch.cuda.empty_cache()
+        Av, Bv = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
+        Cv = torch.empty((n, n), dtype=torch.float64, device=dev)
+        with mf.Plan(triple, 3, n, device=local) as p3:
+            for _ in range(a.warmup):
+                p3.dgemm(Av, Bv, Cv)
+            torch.cuda.synchronize()
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(a.steps):
+                p3.dgemm(Av, Bv, Cv)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            vms = v0.elapsed_time(v1) / a.steps
+        Cr = torch.matmul(Av, Bv)
+        den = n * float(Av.abs().max()) * float(Bv.abs().max())
+        err3 = float((Cv - Cr).abs().max()) / den
+        out["variants"] = [{"workload": f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)",
+                            "value": 2.0 * n ** 3 / (vms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": vms,
+                            "max_scaled_error": err3, "error_bound": 3e-13,
+                            "speedup_vs_cublas": (out.get("classical", {}).get("cublas_ms", 0) / vms) or None}]
+        del Av, Bv, Cv, Cr
 
     if rank == 0 and world == 1 and not a.no_cpu:
         out["cpu_baseline"] = cpu_baseline(a)
