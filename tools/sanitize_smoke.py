@@ -1,0 +1,50 @@
+"""Small workloads touching every kernel path, for compute-sanitizer runs
+(memcheck / racecheck / synccheck, one tool per call):
+flattened + Kronecker-factored + generic K4/K6, leaf BN=128/64 and the simple
+leaf, ragged and odd sizes, host pipeline, level-by-level, sharded plans."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import mf_inputs  # noqa: E402
+import paper_2312_12732_b200 as mf  # noqa: E402
+
+T = mf.triples
+
+
+def run(t, levels, n, **kw):
+    A, B = mf_inputs.pair("int8", n, n)
+    exact = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    host_path = kw.pop("host", False)
+    with mf.Plan(t, levels, n, **kw) as p:
+        if host_path:
+            C = p.dgemm_host(A, B)
+        else:
+            C = p.dgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+    assert (C == exact).all(), (t.name if t else "classical", levels, n, kw)
+
+
+run(None, 0, 256)                        # leaf BN=128/64 decided by wave model
+run(None, 0, 33)                         # simple leaf (odd m)
+run(T.STRASSEN_WINOGRAD, 1, 400)         # ragged m=200
+run(T.STRASSEN_WINOGRAD, 2, 256)         # flattened fixed K4/K6
+run(T.STRASSEN_WINOGRAD, 3, 256)         # Kronecker-factored K4/K6
+run(T.LADERMAN, 1, 288)
+run(T.LADERMAN, 2, 144)                  # factored, p=3
+os.environ["MF_MIX_GENERIC"] = "1"
+run(T.STRASSEN_WINOGRAD, 2, 256)         # generic table-driven K4/K6
+del os.environ["MF_MIX_GENERIC"]
+run(T.STRASSEN_WINOGRAD, 2, 1024, host=True)   # host pipeline (regions, 4 streams)
+run(T.STRASSEN_WINOGRAD, 2, 256, level_by_level=True)
+n = 1024
+A, B = mf_inputs.pair("int8", n, 1)
+tot = np.zeros((n, n))
+for r in range(3):                        # split sharding
+    with mf.Plan(T.STRASSEN_WINOGRAD, 2, n, shard_rank=r, shard_count=3) as p:
+        tot += p.dgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
+assert (tot == (A.astype(np.int64) @ B.astype(np.int64))).all()
+torch.cuda.synchronize()
+print("sanitize smoke ok")
