@@ -37,7 +37,10 @@ CPU_SAMPLE_N = 4096  # oracle sample: same triple and levels at n/4 (1/64 of the
 
 def cpu_sample_n(a):
     """n of the bounded oracle sample: n/4 capped at 4096, divisible by p^levels."""
-    p = {"laderman": 3, "classical-p3": 3}.get(a.triple, 2) ** a.levels
+    p = 1
+    for part in a.triple.split("(x)"):
+        p *= {"laderman": 3, "classical-p3": 3}.get(part, 2)
+    p = p ** a.levels
     ns = min(max(a.n // 4, p), CPU_SAMPLE_N)
     return max(p, ns - ns % p)
 
@@ -55,7 +58,18 @@ CONFIGS = {
     "x-sw3-16384": (16384, "strassen-winograd", 3),
     "x-ld2-13824": (13824, "laderman", 2),
     "x-sw3-32768": (32768, "strassen-winograd", 3),
+    # mixed chains <6,6,6;161>: 2-then-3 and 3-then-2
+    "x-swld-13824": (13824, "strassen-winograd(x)laderman", 1),
+    "x-ldsw-13824": (13824, "laderman(x)strassen-winograd", 1),
 }
+
+
+def resolve_triple(mf, name):
+    """A catalog name, or 'outer(x)inner' for a one-level mixed chain."""
+    if "(x)" in name:
+        o, i = name.split("(x)")
+        return mf.triples.kron(mf.triples.get(o), mf.triples.get(i))
+    return mf.triples.get(name)
 
 
 def parse():
@@ -88,8 +102,12 @@ def workload_name(a):
 
 
 def _rank(a):
-    return {"strassen-winograd": 7, "paper-strassen": 7, "strassen-1969": 7, "laderman": 23,
-            "classical-p2": 8, "classical-p3": 27}[a.triple]
+    ranks = {"strassen-winograd": 7, "paper-strassen": 7, "strassen-1969": 7, "laderman": 23,
+             "classical-p2": 8, "classical-p3": 27}
+    r = 1
+    for part in a.triple.split("(x)"):
+        r *= ranks[part]
+    return r
 
 
 def config(a, world):
@@ -166,6 +184,15 @@ def leaf_traffic():
     return None
 
 
+def oracle_triple(a):
+    import oracle
+    parts = [oracle.catalog(x) for x in a.triple.split("(x)")]
+    t = parts[0]
+    for x in parts[1:]:
+        t = oracle.kron(t, x)
+    return t
+
+
 def cpu_baseline(a):
     """The oracle (or_fmm: plain C interpreter of Eq. "strassen", OpenMP over
     rows) on the host cores: same triple and levels at n = CPU_SAMPLE_N."""
@@ -174,7 +201,7 @@ def cpu_baseline(a):
     import oracle
     n = cpu_sample_n(a)
     A, B = mf_inputs.pair("uniform", n, 0)
-    t = oracle.catalog(a.triple)
+    t = oracle_triple(a)
     t0 = time.perf_counter()
     oracle.fmm(A, B, t, a.levels)
     dt = time.perf_counter() - t0
@@ -194,7 +221,7 @@ def run_reference(a):
     import oracle
     n = cpu_sample_n(a)
     A, B = mf_inputs.pair("uniform", n, 0)
-    t = oracle.catalog(a.triple)
+    t = oracle_triple(a)
     for _ in range(a.warmup):
         oracle.fmm(A, B, t, a.levels)
     times = []
@@ -241,7 +268,7 @@ def main():
         comm = mf.nccl_comm_create(obj[0], rank, world)
 
     n = a.n
-    triple = mf.triples.get(a.triple)
+    triple = resolve_triple(mf, a.triple)
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
                    nccl_comm=comm, profile=True, level_by_level=a.level_by_level)
     info = plan.info()
@@ -284,7 +311,7 @@ def main():
     leaf_ms = phases["leaf"] / max(1, phases["calls"])
     leaf_flops = my_prods * 2.0 * m ** 3
     if a.level_by_level:  # the leaf phase holds the whole sub-recursion of each product
-        R, p = _rank(a), {"laderman": 3}.get(a.triple, 2)
+        R, p = _rank(a), triple.p
         leaf_flops = R ** a.levels * 2.0 * (n // p ** a.levels) ** 3
     peak, peak_src = fp64_peak()
     achieved = leaf_flops / (leaf_ms * 1e-3) / 1e12

@@ -1,8 +1,9 @@
 // mf_kron.cu -- K4/K6 for Kronecker powers of a catalog triple, evaluated
 // level by level (Kronecker-factored) instead of over the flattened table.
 //
-// For <U,V,W> = <u,v,w>^(x)L the flattened combination
-//   T_(q1..qL) = sum_(k1..kL) u[k1][q1]...u[kL][qL] A_(k1..kL)
+// For <U,V,W> = <u1,v1,w1> (x) ... (x) <uL,vL,wL> (a power
+// or a mixed chain such as SW (x) Laderman) the flattened combination
+//   T_(q1..qL) = sum_(k1..kL) u1[k1][q1]...uL[kL][qL] A_(k1..kL)
 // factors into L small combinations.  Evaluated OUTER level first for K4
 // and INNER level first for K6, this is exactly the order the paper's
 // recursion uses ("compute the operands T_i and S_i first,
@@ -18,6 +19,7 @@
 // registers), and walks the level tree with the intermediate sums in
 // registers.  Accumulators start at -0.0 (bitwise the first-term rule).
 #include <cstdint>
+#include <tuple>
 #include <utility>
 
 #include "mf_internal.h"
@@ -28,14 +30,48 @@ namespace kronmix {
 
 using fixed::Tri;
 
-template <int B, int E>
-struct ipow { static constexpr int v = B * ipow<B, E - 1>::v; };
-template <int B>
-struct ipow<B, 0> { static constexpr int v = 1; };
+// A chain of base triples, outermost first: <u1,v1,w1> (x) <u2,v2,w2> (x) ...
+// (a power is the chain of one triple repeated).
+template <class... Ts>
+struct Chain {
+  static constexpr int L = sizeof...(Ts);
+  // per-level p and R as pure functions (no static arrays: usable at run time
+  // in device code, e.g. in flat_block's loop)
+  __host__ __device__ static constexpr int p_of(int l) {
+    int v = 0, i = 0;
+    ((v = (i++ == l) ? Ts::p : v), ...);
+    return v;
+  }
+  __host__ __device__ static constexpr int R_of(int l) {
+    int v = 0, i = 0;
+    ((v = (i++ == l) ? Ts::R : v), ...);
+    return v;
+  }
+  template <int LEV>  // 0-based
+  using tag = std::tuple_element_t<LEV, std::tuple<Ts...>>;
+  __host__ __device__ static constexpr int NB(int lev) { return p_of(lev) * p_of(lev); }
+  __host__ __device__ static constexpr int NB_from(int lev) {  // prod_{l >= lev} p_l^2
+    int v = 1;
+    for (int l = lev; l < L; ++l) v *= p_of(l) * p_of(l);
+    return v;
+  }
+  __host__ __device__ static constexpr int R_from(int lev) {
+    int v = 1;
+    for (int l = lev; l < L; ++l) v *= R_of(l);
+    return v;
+  }
+  __host__ __device__ static constexpr int P() {
+    int v = 1;
+    for (int l = 0; l < L; ++l) v *= p_of(l);
+    return v;
+  }
+};
 
-// base coefficient (side 0: U, 1: V, 2: W) as a compile-time scalar
-template <class Tag, int SIDE, int K, int Q>
-inline constexpr int coef = SIDE == 0 ? Tag::T.U[K][Q] : (SIDE == 1 ? Tag::T.V[K][Q] : Tag::T.W[K][Q]);
+// base coefficient of level LEV's triple (side 0: U, 1: V, 2: W)
+template <class Ch, int LEV, int SIDE, int K, int Q>
+inline constexpr int coef = SIDE == 0   ? Ch::template tag<LEV>::T.U[K][Q]
+                            : SIDE == 1 ? Ch::template tag<LEV>::T.V[K][Q]
+                                        : Ch::template tag<LEV>::T.W[K][Q];
 
 template <int NB, int R>
 constexpr bool single(const int8_t (&M)[NB][R], int q) {  // one +-1 entry
@@ -51,36 +87,39 @@ constexpr bool single_pos(const int8_t (&M)[NB][R], int q) {
   return true;
 }
 
-// Flattened product q (base-R digits q1..qL, outer first) aliases its A (B)
-// block iff every level's column is a single +-1 (mf_plan's rule).
-template <class Tag, int SIDE, int L>
+template <class Tag, int SIDE>
+constexpr bool single_col(int q) { return single(SIDE == 0 ? Tag::T.U : Tag::T.V, q); }
+
+template <class Ch, int SIDE, size_t... Ls>
+constexpr bool aliased_impl(int q, std::index_sequence<Ls...>) {
+  // digits of q, innermost last: q = (..((q0)*R1 + q1)*R2 + ..)
+  int digits[Ch::L] = {};
+  for (int l = Ch::L - 1; l >= 0; --l) { digits[l] = q % Ch::R_of(l); q /= Ch::R_of(l); }
+  return (single_col<typename Ch::template tag<Ls>, SIDE>(digits[Ls]) && ...);
+}
+// flattened product q aliases its A (B) block iff every level's column is a
+// single +-1 (mf_plan's rule)
+template <class Ch, int SIDE>
 constexpr bool aliased(int q) {
-  constexpr int R = Tag::R;
-  for (int l = 0; l < L; ++l) {
-    const int ql = q % R;
-    q /= R;
-    if (!single(SIDE == 0 ? Tag::T.U : Tag::T.V, ql)) return false;
-  }
-  return true;
+  return aliased_impl<Ch, SIDE>(q, std::make_index_sequence<Ch::L>{});
 }
 
-template <class Tag, int SIDE, int L>
+template <class Ch, int SIDE>
 struct Slots {
-  int slot[ipow<Tag::R, L>::v];
+  int slot[Ch::R_from(0)];
 };
-template <class Tag, int SIDE, int L>
-constexpr Slots<Tag, SIDE, L> make_slots() {
-  Slots<Tag, SIDE, L> s{};
+template <class Ch, int SIDE>
+constexpr Slots<Ch, SIDE> make_slots() {
+  Slots<Ch, SIDE> s{};
   int next = 0;
-  for (int q = 0; q < ipow<Tag::R, L>::v; ++q) s.slot[q] = aliased<Tag, SIDE, L>(q) ? -1 : next++;
+  for (int q = 0; q < Ch::R_from(0); ++q) s.slot[q] = aliased<Ch, SIDE>(q) ? -1 : next++;
   return s;
 }
-template <class Tag, int SIDE, int L>
-inline constexpr Slots<Tag, SIDE, L> slots_v = make_slots<Tag, SIDE, L>();
-template <class Tag, int SIDE, int L, int Q>
-inline constexpr int slot_v = slots_v<Tag, SIDE, L>.slot[Q];
+template <class Ch, int SIDE>
+inline constexpr Slots<Ch, SIDE> slots_v = make_slots<Ch, SIDE>();
+template <class Ch, int SIDE, int Q>
+inline constexpr int slot_v = slots_v<Ch, SIDE>.slot[Q];
 
-// the catalog triples fold no signs (every single-entry column is +1)
 template <class Tag>
 constexpr bool unsigned_aliases_f() {
   for (int q = 0; q < Tag::R; ++q) {
@@ -89,21 +128,26 @@ constexpr bool unsigned_aliases_f() {
   }
   return true;
 }
-template <class Tag>
-inline constexpr bool unsigned_aliases = unsigned_aliases_f<Tag>();
+// the catalog triples fold no signs (every single-entry column is +1)
+template <class... Ts>
+constexpr bool chain_unsigned(Chain<Ts...>*) { return (unsigned_aliases_f<Ts>() && ...); }
+template <class Ch>
+inline constexpr bool unsigned_aliases = chain_unsigned(static_cast<Ch*>(nullptr));
 
-// flat block index of digit tuple idx (base NB1 digits k1..kL, outer first)
-template <int P1, int L>
+// flat block index (row * P + col) of the digit tuple idx = (k1..kL), k_l in
+// [0, p_l^2), outer first (SPEC.md L244's interleave, applied per level)
+template <class Ch>
 __host__ __device__ constexpr int flat_block(int idx) {
   int row = 0, col = 0, scale = 1;
-  for (int l = 0; l < L; ++l) {  // innermost digit first
-    const int k = idx % (P1 * P1);
-    idx /= P1 * P1;
-    row += (k / P1) * scale;
-    col += (k % P1) * scale;
-    scale *= P1;
+  for (int l = Ch::L - 1; l >= 0; --l) {  // innermost digit first
+    const int p = Ch::p_of(l);
+    const int k = idx % (p * p);
+    idx /= p * p;
+    row += (k / p) * scale;
+    col += (k % p) * scale;
+    scale *= p;
   }
-  return row * scale + col;  // scale == P1^L == P
+  return row * scale + col;
 }
 
 template <int VW> struct V { double v[VW]; };
@@ -142,33 +186,32 @@ __device__ __forceinline__ void st1(double* p, const V<VW>& x) {
 }
 
 // ---------------------------------------------------------------- K4
-// Level LEV (1-based) of the pre-addition tree under product prefix QP:
-// in[] holds NB1^(L-LEV+1) values indexed (k_LEV, k_LEV+1..k_L).
-template <class Tag, int L, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
+// Level LEV (0-based) of the pre-addition tree under product prefix QP:
+// in[] holds NB_from(LEV) values indexed (k_LEV, k_LEV+1..k_L-1).
+template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
 __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64_t off, int64_t mm,
                                       std::integer_sequence<int, Ks...>);
 
-template <class Tag, int L, int SIDE, int VW, int LEV, int QP, int NIN, int... Qs>
+template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int... Qs>
 __device__ __forceinline__ void pre_stage(const V<VW> (&in)[NIN], double* out, int64_t off,
                                           int64_t mm, std::integer_sequence<int, Qs...>) {
-  constexpr int NB1 = Tag::p * Tag::p;
-  (pre_q<Tag, L, SIDE, VW, LEV, QP, NIN, Qs>(in, out, off, mm, std::make_integer_sequence<int, NB1>{}),
+  (pre_q<Ch, SIDE, VW, LEV, QP, NIN, Qs>(in, out, off, mm,
+                                         std::make_integer_sequence<int, Ch::NB(LEV)>{}),
    ...);
 }
 
-template <class Tag, int L, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
+template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
 __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64_t off, int64_t mm,
                                       std::integer_sequence<int, Ks...>) {
-  constexpr int NB1 = Tag::p * Tag::p;
-  constexpr int NOUT = NIN / NB1;
-  constexpr int q = QP * Tag::R + Q;
-  if constexpr (LEV == L) {
-    if constexpr (slot_v<Tag, SIDE, L, q> >= 0) {
+  constexpr int NOUT = NIN / Ch::NB(LEV);
+  constexpr int q = QP * Ch::R_of(LEV) + Q;
+  if constexpr (LEV == Ch::L - 1) {
+    if constexpr (slot_v<Ch, SIDE, q> >= 0) {
       V<VW> y;
 #pragma unroll
       for (int e = 0; e < VW; ++e) y.v[e] = -0.0;
-      (acc_term<coef<Tag, SIDE, Ks, Q>, VW>(y, in[Ks]), ...);
-      st1<VW>(out + (int64_t)slot_v<Tag, SIDE, L, q> * mm + off, y);
+      (acc_term<coef<Ch, LEV, SIDE, Ks, Q>, VW>(y, in[Ks]), ...);
+      st1<VW>(out + (int64_t)slot_v<Ch, SIDE, q> * mm + off, y);
     }
   } else {
     V<VW> y[NOUT];
@@ -176,21 +219,20 @@ __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64
     for (int kk = 0; kk < NOUT; ++kk) {
 #pragma unroll
       for (int e = 0; e < VW; ++e) y[kk].v[e] = -0.0;
-      (acc_term<coef<Tag, SIDE, Ks, Q>, VW>(y[kk], in[Ks * NOUT + kk]), ...);
+      (acc_term<coef<Ch, LEV, SIDE, Ks, Q>, VW>(y[kk], in[Ks * NOUT + kk]), ...);
     }
-    pre_stage<Tag, L, SIDE, VW, LEV + 1, q, NOUT>(y, out, off, mm,
-                                                  std::make_integer_sequence<int, Tag::R>{});
+    pre_stage<Ch, SIDE, VW, LEV + 1, q, NOUT>(y, out, off, mm,
+                                              std::make_integer_sequence<int, Ch::R_of(LEV + 1)>{});
   }
 }
 
-template <class Tag, int L, int SIDE, int VW>
+template <class Ch, int SIDE, int VW>
 __global__ void __launch_bounds__(256) premix_kron(const double* __restrict__ X, int64_t ldx,
                                                    int64_t m, double* __restrict__ out, int64_t r0,
                                                    int64_t r1, int64_t c0, int64_t c1) {
-  static_assert(unsigned_aliases<Tag>, "sign folding not supported on this path");
-  constexpr int NB1 = Tag::p * Tag::p;
-  constexpr int NB = ipow<NB1, L>::v;
-  constexpr int P = ipow<Tag::p, L>::v;
+  static_assert(unsigned_aliases<Ch>, "sign folding not supported on this path");
+  constexpr int NB = Ch::NB_from(0);
+  constexpr int P = Ch::P();
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
@@ -201,66 +243,64 @@ __global__ void __launch_bounds__(256) premix_kron(const double* __restrict__ X,
     V<VW> x[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
-      const int b = flat_block<Tag::p, L>(k);
+      const int b = flat_block<Ch>(k);
       x[k] = ld1<VW>(X + ((b / P) * m + r) * ldx + (b % P) * m + c);
     }
-    pre_stage<Tag, L, SIDE, VW, 1, 0, NB>(x, out, r * m + c, mm,
-                                           std::make_integer_sequence<int, Tag::R>{});
+    pre_stage<Ch, SIDE, VW, 0, 0, NB>(x, out, r * m + c, mm,
+                                      std::make_integer_sequence<int, Ch::R_of(0)>{});
   }
 }
 
 // ---------------------------------------------------------------- K6
-// Level LEV of the post-addition tree under prefix QP: acc[] holds
-// NB1^(L-LEV+1) partial C values indexed (i_LEV, i_LEV+1..i_L); the deepest
-// level combines leaf products over q_L, each shallower level combines the
-// level below over its q (inner first, as the recursion distributes P_i).
-template <class Tag, int L, int VW, int LEV, int QP, int NACC, int Q, int... Is>
+// Level LEV of the post-addition tree under prefix QP: acc[] holds NB_from(LEV)
+// partial C values indexed (i_LEV, i_LEV+1..); the deepest level combines leaf
+// products over its q, each shallower level combines the level below (inner
+// first, as the recursion distributes P_i).
+template <class Ch, int VW, int LEV, int QP, int NACC, int Q, int... Is>
 __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
                                        int64_t off, int64_t mm, std::integer_sequence<int, Is...>);
 
-template <class Tag, int L, int VW, int LEV, int QP, int NACC, int... Qs>
+template <class Ch, int VW, int LEV, int QP, int NACC, int... Qs>
 __device__ __forceinline__ void post_stage(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
                                            int64_t off, int64_t mm,
                                            std::integer_sequence<int, Qs...>) {
-  constexpr int NB1 = Tag::p * Tag::p;
-  (post_q<Tag, L, VW, LEV, QP, NACC, Qs>(acc, Pw, off, mm, std::make_integer_sequence<int, NB1>{}),
+  (post_q<Ch, VW, LEV, QP, NACC, Qs>(acc, Pw, off, mm, std::make_integer_sequence<int, Ch::NB(LEV)>{}),
    ...);
 }
 
-template <class Tag, int L, int VW, int LEV, int QP, int NACC, int Q, int... Is>
+template <class Ch, int VW, int LEV, int QP, int NACC, int Q, int... Is>
 __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
                                        int64_t off, int64_t mm, std::integer_sequence<int, Is...>) {
-  constexpr int NB1 = Tag::p * Tag::p;
-  constexpr int NSUB = NACC / NB1;
-  constexpr int q = QP * Tag::R + Q;
-  constexpr int nz = (0 + ... + (coef<Tag, 2, Is, Q> != 0));
+  constexpr int NSUB = NACC / Ch::NB(LEV);
+  constexpr int q = QP * Ch::R_of(LEV) + Q;
+  constexpr int nz = (0 + ... + (coef<Ch, LEV, 2, Is, Q> != 0));
   if constexpr (nz > 0) {
-    if constexpr (LEV == L) {
+    if constexpr (LEV == Ch::L - 1) {
       const V<VW> x = ld1<VW>(Pw + (int64_t)q * mm + off);
-      (acc_term<coef<Tag, 2, Is, Q>, VW>(acc[Is], x), ...);
+      (acc_term<coef<Ch, LEV, 2, Is, Q>, VW>(acc[Is], x), ...);
     } else {
       V<VW> y[NSUB];
 #pragma unroll
       for (int rr = 0; rr < NSUB; ++rr)
 #pragma unroll
         for (int e = 0; e < VW; ++e) y[rr].v[e] = -0.0;
-      post_stage<Tag, L, VW, LEV + 1, q, NSUB>(y, Pw, off, mm,
-                                               std::make_integer_sequence<int, Tag::R>{});
+      post_stage<Ch, VW, LEV + 1, q, NSUB>(y, Pw, off, mm,
+                                           std::make_integer_sequence<int, Ch::R_of(LEV + 1)>{});
 #pragma unroll
-      for (int rr = 0; rr < NSUB; ++rr) (acc_term<coef<Tag, 2, Is, Q>, VW>(acc[Is * NSUB + rr], y[rr]), ...);
+      for (int rr = 0; rr < NSUB; ++rr)
+        (acc_term<coef<Ch, LEV, 2, Is, Q>, VW>(acc[Is * NSUB + rr], y[rr]), ...);
     }
   }
 }
 
-template <class Tag, int L, int VW>
+template <class Ch, int VW>
 __global__ void __launch_bounds__(256) postmix_kron(const double* __restrict__ Pw, int64_t m,
                                                     double alpha, double* __restrict__ C,
                                                     int64_t ldc, int64_t r0, int64_t r1, int64_t c0,
                                                     int64_t c1) {
-  static_assert(unsigned_aliases<Tag>, "sign folding not supported on this path");
-  constexpr int NB1 = Tag::p * Tag::p;
-  constexpr int NB = ipow<NB1, L>::v;
-  constexpr int P = ipow<Tag::p, L>::v;
+  static_assert(unsigned_aliases<Ch>, "sign folding not supported on this path");
+  constexpr int NB = Ch::NB_from(0);
+  constexpr int P = Ch::P();
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
@@ -273,15 +313,15 @@ __global__ void __launch_bounds__(256) postmix_kron(const double* __restrict__ P
     for (int i = 0; i < NB; ++i)
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc[i].v[e] = -0.0;
-    post_stage<Tag, L, VW, 1, 0, NB>(acc, Pw, r * m + c, mm,
-                                      std::make_integer_sequence<int, Tag::R>{});
+    post_stage<Ch, VW, 0, 0, NB>(acc, Pw, r * m + c, mm,
+                                 std::make_integer_sequence<int, Ch::R_of(0)>{});
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       if (alpha != 1.0) {
 #pragma unroll
         for (int e = 0; e < VW; ++e) acc[i].v[e] = __dmul_rn(alpha, acc[i].v[e]);
       }
-      const int b = flat_block<Tag::p, L>(i);
+      const int b = flat_block<Ch>(i);
       st1<VW>(C + ((b / P) * m + r) * ldc + (b % P) * m + c, acc[i]);
     }
   }
@@ -296,64 +336,84 @@ int grid_for(int64_t work) {
   return (int)(blocks < cap ? (blocks < 1 ? 1 : blocks) : cap);
 }
 
-// host-side Kronecker power of a base table, compared with the plan's
+// host side: is the plan's flattened triple the chain's Kronecker product?
 template <class Tag>
-bool is_power(const Plan& pl, int L) {
-  const int p = Tag::p, R = Tag::R, NB1 = p * p;
-  int P = 1, RL = 1;
-  for (int l = 0; l < L; ++l) { P *= p; RL *= R; }
-  if (pl.P != P || pl.RL != RL) return false;
+int base_coef(int side, int k, int q) {
+  return side == 0 ? Tag::T.U[k][q] : (side == 1 ? Tag::T.V[k][q] : Tag::T.W[k][q]);
+}
+template <class... Ts>
+bool is_chain(const Plan& pl) {
+  using Ch = Chain<Ts...>;
+  constexpr int L = Ch::L;
+  if (pl.P != Ch::P() || pl.RL != Ch::R_from(0)) return false;
+  int (*coefs[L])(int, int, int) = {&base_coef<Ts>...};
+  const int P = Ch::P(), RL = Ch::R_from(0);
   for (int idx = 0; idx < P * P; ++idx) {
-    // digits of flat block idx (row, col) -> per-level base blocks, outer first
-    int row = idx / P, col = idx % P;
-    int k[8];
-    for (int l = L - 1; l >= 0; --l) { k[l] = (row % p) * p + (col % p); row /= p; col /= p; }
-    (void)NB1;
+    int row = idx / P, col = idx % P, k[L];
+    for (int l = L - 1; l >= 0; --l) {
+      const int p = Ch::p_of(l);
+      k[l] = (row % p) * p + (col % p);
+      row /= p;
+      col /= p;
+    }
     for (int q = 0; q < RL; ++q) {
-      int qq = q, u = 1, v = 1, w = 1;
+      int qq = q, c[3] = {1, 1, 1};
       for (int l = L - 1; l >= 0; --l) {
-        const int ql = qq % R;
-        qq /= R;
-        u *= Tag::T.U[k[l]][ql];
-        v *= Tag::T.V[k[l]][ql];
-        w *= Tag::T.W[k[l]][ql];
+        const int ql = qq % Ch::R_of(l);
+        qq /= Ch::R_of(l);
+        for (int sd = 0; sd < 3; ++sd) c[sd] *= coefs[l](sd, k[l], ql);
       }
       const size_t at = (size_t)idx * RL + q;
-      if (pl.U[at] != u || pl.V[at] != v || pl.W[at] != w) return false;
+      if (pl.U[at] != c[0] || pl.V[at] != c[1] || pl.W[at] != c[2]) return false;
     }
   }
   return true;
 }
+
+using fixed::TagLD;
+using fixed::TagPS;
+using fixed::TagS69;
+using fixed::TagSW;
+using ChSW3 = Chain<TagSW, TagSW, TagSW>;
+using ChPS3 = Chain<TagPS, TagPS, TagPS>;
+using ChS693 = Chain<TagS69, TagS69, TagS69>;
+using ChLD2 = Chain<TagLD, TagLD>;
+using ChSWLD = Chain<TagSW, TagLD>;
+using ChLDSW = Chain<TagLD, TagSW>;
 
 }  // namespace kronmix
 
 // ids 8.. : Kronecker-factored kernels (see mf_fixed.cu for 1..7)
 int kron_match(const Plan& pl) {
   using namespace kronmix;
-  if (pl.P == 8 && is_power<fixed::TagSW>(pl, 3)) return 8;
-  if (pl.P == 8 && is_power<fixed::TagPS>(pl, 3)) return 9;
-  if (pl.P == 8 && is_power<fixed::TagS69>(pl, 3)) return 10;
-  if (pl.P == 9 && is_power<fixed::TagLD>(pl, 2)) return 11;
+  if (is_chain<TagSW, TagSW, TagSW>(pl)) return 8;
+  if (is_chain<TagPS, TagPS, TagPS>(pl)) return 9;
+  if (is_chain<TagS69, TagS69, TagS69>(pl)) return 10;
+  if (is_chain<TagLD, TagLD>(pl)) return 11;
+  if (is_chain<TagSW, TagLD>(pl)) return 12;
+  if (is_chain<TagLD, TagSW>(pl)) return 13;
   return 0;
 }
 
-#define MF_KRON_SWITCH(ID, CALL)          \
-  switch (ID) {                           \
-    case 8: return CALL(fixed::TagSW, 3); \
-    case 9: return CALL(fixed::TagPS, 3); \
-    case 10: return CALL(fixed::TagS69, 3); \
-    case 11: return CALL(fixed::TagLD, 2); \
-    default: return cudaErrorInvalidValue; \
+#define MF_KRON_SWITCH(ID, CALL)             \
+  switch (ID) {                              \
+    case 8: return CALL(kronmix::ChSW3);     \
+    case 9: return CALL(kronmix::ChPS3);     \
+    case 10: return CALL(kronmix::ChS693);   \
+    case 11: return CALL(kronmix::ChLD2);    \
+    case 12: return CALL(kronmix::ChSWLD);   \
+    case 13: return CALL(kronmix::ChLDSW);   \
+    default: return cudaErrorInvalidValue;   \
   }
 
 cudaError_t launch_premix_kron(int id, int side, const double* X, int64_t ldx, int64_t m,
                                double* out, cudaStream_t s, Rows rows) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   const int grid = kronmix::grid_for((r1 - r0) * (c1 - c0));
-#define PRE(T_, L_)                                                                                \
-  (side == 0 ? (kronmix::premix_kron<T_, L_, 0, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
-                cudaGetLastError())                                                                \
-             : (kronmix::premix_kron<T_, L_, 1, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
+#define PRE(CH_)                                                                                  \
+  (side == 0 ? (kronmix::premix_kron<CH_, 0, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
+                cudaGetLastError())                                                               \
+             : (kronmix::premix_kron<CH_, 1, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
                 cudaGetLastError()))
   MF_KRON_SWITCH(id, PRE)
 #undef PRE
@@ -363,8 +423,8 @@ cudaError_t launch_postmix_kron(int id, const double* Pw, int64_t m, double alph
                                 int64_t ldc, cudaStream_t s, Rows rows) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   const int grid = kronmix::grid_for((r1 - r0) * (c1 - c0));
-#define POST(T_, L_)                                                                              \
-  (kronmix::postmix_kron<T_, L_, 1><<<grid, 256, 0, s>>>(Pw, m, alpha, C, ldc, r0, r1, c0, c1), \
+#define POST(CH_)                                                                              \
+  (kronmix::postmix_kron<CH_, 1><<<grid, 256, 0, s>>>(Pw, m, alpha, C, ldc, r0, r1, c0, c1), \
    cudaGetLastError())
   MF_KRON_SWITCH(id, POST)
 #undef POST

@@ -129,6 +129,24 @@ def classical(p: int) -> Triple:
     return _t(f"classical-p{p}", p, U, V, W)
 
 
+def kron(outer: Triple, inner: Triple) -> Triple:
+    """One level of the chain outer-then-inner as a single triple (PAPER.md
+    L303-313: a (x) a', b (x) b', c (x) c').  Block (b of outer, s of inner) ->
+    row-major block ((b/po)*pi + s/pi, (b%po)*pi + s%pi) of the (po*pi)-way
+    split; product q = q_outer * R_inner + q_inner.  Pass the
+    result to Plan with levels=1; mf_plan re-proves it (Brent) before use."""
+    po, pi = outer.p, inner.p
+    P, R = po * pi, outer.R * inner.R
+    U = np.zeros((P * P, R)); V = np.zeros((P * P, R)); W = np.zeros((P * P, R))
+    for b in range(po * po):
+        for s in range(pi * pi):
+            row = ((b // po) * pi + s // pi) * P + (b % po) * pi + s % pi
+            U[row] = np.kron(outer.U[b], inner.U[s])
+            V[row] = np.kron(outer.V[b], inner.V[s])
+            W[row] = np.kron(outer.W[b], inner.W[s])
+    return _t(f"{outer.name}(x){inner.name}", P, U, V, W)
+
+
 CATALOG = {t.name: t for t in (STRASSEN_WINOGRAD, PAPER_STRASSEN, STRASSEN_1969, LADERMAN,
                                classical(2), classical(3))}
 

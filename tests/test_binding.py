@@ -153,3 +153,14 @@ def test_host_only_split_sharding_exact_balance(N):
     assert slabs[0][0] == 0 and slabs[-1][1] == m
     assert all(slabs[i][1] == slabs[i + 1][0] for i in range(N - 1))
     assert all(a % 128 == 0 for a, _ in slabs)
+
+
+def test_product_kron_matches_oracle_kron():
+    """triples.kron (product side) and or_kron (oracle) agree for the mixed chains
+    of PAPER.md L275-278 (6 = 2x3 and 3x2 as 7*23 products)."""
+    for o, i in (("strassen-winograd", "laderman"), ("laderman", "strassen-winograd"),
+                 ("strassen-winograd", "strassen-winograd")):
+        a = triples.kron(triples.get(o), triples.get(i))
+        b = oracle.kron(oracle.catalog(o), oracle.catalog(i))
+        assert a.p == b.p and a.R == b.R
+        assert (a.U == b.U).all() and (a.V == b.V).all() and (a.W == b.W).all()

@@ -168,23 +168,28 @@ def test_postmix_bit_exact(name, levels, n, path, monkeypatch):
 
 def _recursive_premix(X, t, levels, side):
     """The oracle's recursion (or_fmm) for the operands: level-1
-    T_q of X, then level-2 T of each, ... -> R^levels blocks, index outer-major."""
+    T_q of X, then level-2 T of each, ... -> R^levels blocks, index outer-major.
+    t may be a list of triples, one per level (a mixed chain), outer first."""
+    chain = t if isinstance(t, list) else [t] * levels
     blocks = [X]
-    for _ in range(levels):
-        blocks = [T for Y in blocks for T in oracle.premix(Y, t, side)]
+    for tl in chain:
+        blocks = [T for Y in blocks for T in oracle.premix(Y, tl, side)]
     return np.stack(blocks)
 
 
 def _recursive_postmix(P, t, levels, n, alpha):
     """The oracle's recursion for the post-addition: combine the innermost level
     first ("recursively solve P_i and distribute it"), alpha last."""
+    chain = t if isinstance(t, list) else [t] * levels
     cur = list(P)
-    size = n // t.p ** levels
-    for lev in range(levels):
-        size *= t.p
-        a = alpha if lev == levels - 1 else 1.0
-        cur = [oracle.postmix(np.stack(cur[g * t.R:(g + 1) * t.R]), t, size, a)
-               for g in range(len(cur) // t.R)]
+    size = n
+    for tl in chain:
+        size //= tl.p
+    for lev, tl in enumerate(reversed(chain)):
+        size *= tl.p
+        a = alpha if lev == len(chain) - 1 else 1.0
+        cur = [oracle.postmix(np.stack(cur[g * tl.R:(g + 1) * tl.R]), tl, size, a)
+               for g in range(len(cur) // tl.R)]
     return cur[0]
 
 
@@ -214,6 +219,38 @@ def test_kron_factored_mix_bit_exact_with_recursion(name, levels, n):
             C = torch.empty((n, n), dtype=torch.float64, device="cuda")
             p.postmix(dev(Pp), C, alpha=alpha)
             assert (host(C) == _recursive_postmix(Pp, to, levels, n, alpha)).all()
+
+
+@pytest.mark.parametrize("outer,inner", [(SW, "laderman"), ("laderman", SW)])
+@pytest.mark.parametrize("n", [72, 1152])
+def test_mixed_chain_6x6(outer, inner, n):
+    """NEXT-2: the chains 2-then-3 and 3-then-2 ("the sequence 2 and 3
+    specifies an algorithm that is different from the sequence 3 and 2") as one
+    flattened <6,6,6;161> level: Kronecker-factored K4/K6 bitwise the oracle's
+    mixed recursion, end to end exact on integers and within the bound."""
+    to, ti = triples.get(outer), triples.get(inner)
+    t = triples.kron(to, ti)
+    chain = [oracle.catalog(outer), oracle.catalog(inner)]
+    assert t.p == 6 and t.R == 161
+    A, B = mf_inputs.pair("uniform", n, 25)
+    with mf.Plan(t, 1, n) as p:
+        info, pr = p.info(), p.products()
+        m = info["leaf_n"]
+        for side, X, src, idx in (("A", A, pr["a_src"], pr["a_idx"]), ("B", B, pr["b_src"], pr["b_idx"])):
+            out = torch.empty((info["n_mat_a"] if side == "A" else info["n_mat_b"], m, m),
+                              dtype=torch.float64, device="cuda")
+            p.premix(side, dev(X), out)
+            got, ref = host(out), _recursive_premix(X, chain, 2, side)
+            for q in np.nonzero(src == 1)[0]:
+                assert (got[idx[q]] == ref[q]).all(), (side, q)
+        Pp = np.random.Generator(np.random.PCG64(26)).uniform(-1, 1, size=(161, m, m))
+        C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        p.postmix(dev(Pp), C, alpha=0.5)
+        assert (host(C) == _recursive_postmix(Pp, chain, 2, n, 0.5)).all()
+        C = host(p.dgemm(dev(A), dev(B)))
+        assert scaled(C, oracle.classical(A, B), A, B) <= 2e-13
+        Ai, Bi = mf_inputs.pair("int1024", n, 27)
+        assert (host(p.dgemm(dev(Ai), dev(Bi))) == exact(Ai, Bi)).all()
 
 
 def test_leaf_stage_matches_oracle_products_on_integers():
