@@ -80,6 +80,11 @@ typedef struct {
                            bilinear map, more HBM passes (an ablation).  With 1,
                            mf_plan_info / mf_plan_products describe the top
                            level (R products, leaf_n = n / p)                    */
+  int64_t max_workspace;  /* bytes; 0 (default) = unlimited.  If the T/S/P workspace
+                           of all products would exceed it, products run in batches
+                           that fit (the paper's OOM at n=24012,
+                           P:L489-492): per batch K4 on its slots, K5, K6 adding
+                           into C.  Unsharded flattened plans only              */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.

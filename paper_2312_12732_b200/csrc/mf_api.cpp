@@ -229,6 +229,9 @@ void free_plan(Plan* pl) {
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
+  for (auto& b : pl->batches)
+    for (void* p : {b.mixA.d_table, b.mixB.d_table, b.mixC.d_table})
+      if (p) cudaFree(p);
   for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
     if (st) cudaStreamDestroy(st);
 }
@@ -253,14 +256,16 @@ bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_
 
 mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
                    const double* T, const double* S, double* out, int64_t ldo, int64_t stride,
-                   double alpha, cudaStream_t s, Rows rows = Rows(), bool part = false) {
+                   double alpha, cudaStream_t s, Rows rows = Rows(), bool part = false,
+                   const Plan::Batch* batch = nullptr) {
   LeafArgs a;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
   a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
   a.P = pl.P; a.m = pl.m;
   a.out = out; a.ldo = ldo; a.out_block_stride = stride; a.alpha = alpha;
-  a.jobs = part ? pl.d_jobs + pl.n_jobs : pl.d_jobs;
-  a.n_jobs = part ? pl.n_jobs_part : pl.n_jobs;
+  a.jobs = batch ? pl.d_jobs + batch->job0 : (part ? pl.d_jobs + pl.n_jobs : pl.d_jobs);
+  a.n_jobs = batch ? batch->n_jobs : (part ? pl.n_jobs_part : pl.n_jobs);
+  if (batch) { a.n_slots_a = batch->n_a; a.n_slots_b = batch->n_b; }
   a.rows = rows;
   MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
   return MF_OK;
@@ -465,6 +470,45 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     if (!pl->my_part.empty()) post_table(pl->mixC2, true);
   }
 
+  // ---- bounded workspace: batches of products whose T/S/P fit the cap ----
+  const int64_t blk = (int64_t)sizeof(double) * pl->m * pl->m;
+  if (levels > 0 && o.max_workspace > 0 &&
+      (int64_t)(pl->n_mat_a + pl->n_mat_b + RL) * blk > o.max_workspace) {
+    if (shard_count > 1)
+      return fail(MF_ERR_UNSUPPORTED, "max_workspace with product sharding is not supported");
+    const int64_t g = o.max_workspace / (3 * blk);
+    if (g < 1)
+      return fail(MF_ERR_OUT_OF_MEMORY, "max_workspace %lld < 3 leaf blocks (%lld bytes)",
+                  (long long)o.max_workspace, (long long)(3 * blk));
+    pl->fixed_id = 0;  // batches use the table-driven K4/K6
+    const int nq = (int)pl->my_prods.size();
+    for (int q0 = 0; q0 < nq; q0 += (int)g) {
+      Plan::Batch b;
+      const int q1 = std::min<int>(nq, q0 + (int)g);
+      const int gb = q1 - q0;
+      b.mixA.nin = b.mixB.nin = NB;
+      b.mixC.nin = gb;
+      b.mixC.nout = NB;
+      b.mixC.coef.assign((size_t)NB * gb, 0.0);
+      for (int i = 0; i < NB; ++i) b.mixC.out_map.push_back(i);
+      for (int j = 0; j < gb; ++j) {
+        const int32_t q = pl->my_prods[q0 + j];
+        const Product& pr = pl->prods[q];
+        for (int side = 0; side < 2; ++side) {
+          if ((side == 0 ? pr.a_src : pr.b_src) != SRC_WORKSPACE) continue;
+          MixTable& t = side == 0 ? b.mixA : b.mixB;
+          const std::vector<double>& M = side == 0 ? pl->U : pl->V;
+          for (int k = 0; k < NB; ++k) t.coef.push_back(M[k * RL + q]);
+          t.out_map.push_back(side == 0 ? b.n_a++ : b.n_b++);
+          ++t.nout;
+        }
+        for (int i = 0; i < NB; ++i) b.mixC.coef[(size_t)i * gb + j] = pl->W[i * RL + q] * pr.sign;
+      }
+      b.n_jobs = gb;
+      pl->batches.push_back(std::move(b));
+    }
+  }
+
   if (host_only) {  // host logic only: no device work, no workspace
     pl->n_jobs = (int)pl->my_prods.size();
     pl->n_jobs_part = (int)pl->my_part.size();
@@ -477,6 +521,13 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   if (levels > 0) {
     size_t tb = sizeof(double) * mm * pl->n_mat_a, sb = sizeof(double) * mm * pl->n_mat_b,
            pb = sizeof(double) * mm * RL;
+    if (!pl->batches.empty()) {
+      int na = 0, nb = 0, np = 0;
+      for (auto& b : pl->batches) {
+        na = std::max(na, b.n_a); nb = std::max(nb, b.n_b); np = std::max(np, b.n_jobs);
+      }
+      tb = sizeof(double) * mm * na; sb = sizeof(double) * mm * nb; pb = sizeof(double) * mm * np;
+    }
     if (tb && cudaMalloc(&pl->T, tb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace T (%zu bytes)", tb); }
     if (sb && cudaMalloc(&pl->S, sb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace S (%zu bytes)", sb); }
     if (cudaMalloc(&pl->Pw, pb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace P (%zu bytes)", pb); }
@@ -485,6 +536,12 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     if ((st = upload_table(pl->mixA)) != MF_OK || (st = upload_table(pl->mixB)) != MF_OK ||
         (st = upload_table(pl->mixC)) != MF_OK || (st = upload_table(pl->mixA2)) != MF_OK ||
         (st = upload_table(pl->mixC2)) != MF_OK) {
+      free_plan(pl.get());
+      return st;
+    }
+    for (auto& b : pl->batches)
+      if ((st = upload_table(b.mixA)) != MF_OK || (st = upload_table(b.mixB)) != MF_OK ||
+          (st = upload_table(b.mixC)) != MF_OK) {
       free_plan(pl.get());
       return st;
     }
@@ -503,6 +560,24 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   }
   pl->n_jobs = (int)pl->my_prods.size();
   pl->n_jobs_part = (int)pl->my_part.size();
+  {  // batch-local jobs: local slot indices, output into the batch's P block j
+    int base = (int)jobs.size(), nq = 0;
+    for (auto& b : pl->batches) {
+      b.job0 = base;
+      int la = 0, lb = 0;
+      for (int j = 0; j < b.n_jobs; ++j) {
+        const Product& pr = pl->prods[pl->my_prods[nq + j]];
+        LeafJob jb;
+        jb.a_coord = pr.a_src == SRC_INPUT ? ((pr.a_idx / pl->P) << 16) | (pr.a_idx % pl->P) : la++;
+        jb.b_coord = pr.b_src == SRC_INPUT ? ((pr.b_idx / pl->P) << 16) | (pr.b_idx % pl->P) : lb++;
+        jb.flags = (pr.a_src == SRC_WORKSPACE ? 1 : 0) | (pr.b_src == SRC_WORKSPACE ? 2 : 0);
+        jb.out_idx = j;
+        jobs.push_back(jb);
+      }
+      nq += b.n_jobs;
+      base += b.n_jobs;
+    }
+  }
   if (!jobs.empty()) {
     if (cudaMalloc(&pl->d_jobs, sizeof(LeafJob) * jobs.size()) != cudaSuccess) {
       free_plan(pl.get());
@@ -610,12 +685,33 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
   }
 
   cudaEvent_t* ev = prof_slot(pl);
+  if (pl->opt.profile) ++pl->prof_calls;
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
   mark(0);
   if (pl->levels == 0) {
     mark(1); mark(2);
     if ((st = run_leaf(*pl, A, lda, B, ldb, nullptr, nullptr, C, ldc, 0, alpha, s)) != MF_OK) return st;
     mark(3);
+  } else if (!pl->batches.empty()) {
+    // bounded workspace: per batch K4(A), K4(B), K5, K6 (adding into C after the first)
+    // (profiling: each batch records its own event set; phases sum over batches)
+    for (size_t bi = 0; bi < pl->batches.size(); ++bi) {
+      const Plan::Batch& b = pl->batches[bi];
+      if (bi > 0 && ev) {
+        mark(4); mark(5);
+        ev = prof_slot(pl);
+        mark(0);
+      }
+      MF_CUDA(launch_premix(*pl, b.mixA, A, lda, pl->T, s), "pre-add A (K4, batch)");
+      mark(1);
+      MF_CUDA(launch_premix(*pl, b.mixB, B, ldb, pl->S, s), "pre-add B (K4, batch)");
+      mark(2);
+      if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s,
+                         Rows(), false, &b)) != MF_OK)
+        return st;
+      mark(3);
+      MF_CUDA(launch_postmix(*pl, b.mixC, alpha, pl->Pw, C, ldc, s, Rows(), bi > 0), "post-add (K6, batch)");
+    }
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
     MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
@@ -703,8 +799,8 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
   }
   if (ms)
     for (int i = 0; i < 5; ++i) ms[i] = sum[i];
-  if (calls) *calls = (int32_t)pl->prof_used;
-  if (reset) pl->prof_used = 0;
+  if (calls) *calls = (int32_t)pl->prof_calls;
+  if (reset) { pl->prof_used = 0; pl->prof_calls = 0; }
   return MF_OK;
 }
 
@@ -722,7 +818,9 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 // overlaps.  Results are bitwise those of mf_dgemm (same kernels, same order
 // per element).
 static int pipeline_slabs(const Plan& pl) {
-  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child) return 1;
+  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
+      !pl.batches.empty())
+    return 1;
   const int64_t tiles = (pl.m + 127) / 128;
   return (int)std::min<int64_t>(8, tiles);
 }
@@ -883,6 +981,7 @@ mf_status mf_premix(mf_plan_t pl, int32_t side, const double* X, int64_t ldx, do
                     void* stream) {
   g_err.clear();
   if (!pl || !X || !out || (side != 0 && side != 1)) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (!pl->batches.empty()) return fail(MF_ERR_UNSUPPORTED, "component entry points need the full workspace");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no pre-additions");
   DeviceGuard guard(pl->device);
@@ -896,6 +995,7 @@ mf_status mf_leaf(mf_plan_t pl, const double* A, int64_t lda, const double* B, i
                   const double* T, const double* S, double* P, void* stream) {
   g_err.clear();
   if (!pl || !A || !B || !P) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (!pl->batches.empty()) return fail(MF_ERR_UNSUPPORTED, "component entry points need the full workspace");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   DeviceGuard guard(pl->device);
   return run_leaf(*pl, A, lda, B, ldb, T, S, P, pl->m, pl->m * pl->m, 1.0,
@@ -906,6 +1006,7 @@ mf_status mf_postmix(mf_plan_t pl, double alpha, const double* P, double* C, int
                      void* stream) {
   g_err.clear();
   if (!pl || !P || !C) return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if (!pl->batches.empty()) return fail(MF_ERR_UNSUPPORTED, "component entry points need the full workspace");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   if (pl->levels == 0) return fail(MF_ERR_INVALID_ARG, "levels = 0 plan has no post-addition");
   DeviceGuard guard(pl->device);

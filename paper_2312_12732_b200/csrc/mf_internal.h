@@ -86,6 +86,14 @@ struct Plan {
   MixTable mixC;                  // post-addition over the whole products (zero coef elsewhere)
   MixTable mixC2;                 // ... plus the split products (used on rows part_rows)
   int n_jobs_part = 0;            // leaf jobs of split products follow the whole ones in d_jobs
+  // bounded workspace (mf_options.max_workspace): product batches with local
+  // slot numbering; each has its own K4/K6 tables and leaf jobs (d_jobs + job0)
+  struct Batch {
+    MixTable mixA, mixB, mixC;
+    int job0 = 0, n_jobs = 0;
+    int n_a = 0, n_b = 0;  // local T / S slots
+  };
+  std::vector<Batch> batches;
   // device memory
   double* T = nullptr;   // n_mat_a x m x m
   double* S = nullptr;   // n_mat_b x m x m
@@ -106,7 +114,8 @@ struct Plan {
   std::vector<cudaEvent_t> pipe_events;
   // phase profiling (mf_options.profile): 6 events per mf_dgemm call
   std::vector<std::vector<cudaEvent_t>> prof_events;
-  size_t prof_used = 0;
+  size_t prof_used = 0;   // event sets recorded (one per call, or per batch)
+  int64_t prof_calls = 0; // mf_dgemm calls since the last reset
 };
 
 // Region [r0, r1) x [c0, c1) of every m x m block a launch covers (the whole
@@ -123,7 +132,8 @@ struct Rows {
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows = Rows());
 cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
-                           double* C, int64_t ldc, cudaStream_t s, Rows rows = Rows());
+                           double* C, int64_t ldc, cudaStream_t s, Rows rows = Rows(),
+                           bool accumulate = false);
 
 struct LeafArgs {
   // operand views: matrices (4-D block view, SRC_INPUT) and workspaces (3-D)

@@ -107,7 +107,8 @@ template <int VW>
 __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
                                                   const void* __restrict__ table, int nrow,
                                                   int nterm, double alpha, int64_t r0,
-                                                  int64_t r1, int64_t c0, int64_t c1) {
+                                                  int64_t r1, int64_t c0, int64_t c1,
+                                                  int accumulate) {
   extern __shared__ __align__(16) uint8_t s_raw[];
   const size_t tbytes = sizeof(MixRow) * nrow + sizeof(MixTerm) * nterm;
   for (size_t i = threadIdx.x; i < tbytes / 8; i += blockDim.x)
@@ -145,7 +146,13 @@ __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
 #pragma unroll
         for (int e = 0; e < VW; ++e) acc.v[e] = __dmul_rn(alpha, acc.v[e]);
       }
-      store_vec<VW>(out.at(row.target, m, r, c), acc);
+      double* dst = out.at(row.target, m, r, c);
+      if (accumulate) {  // bounded-workspace batches after the first: C += batch sum
+        const Vec<VW> old = load_vec<VW>(dst);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc.v[e] = __dadd_rn(old.v[e], acc.v[e]);
+      }
+      store_vec<VW>(dst, acc);
     }
   }
 }
@@ -164,7 +171,7 @@ int grid_for(int64_t work, int per_block) {
 
 template <int VW>
 cudaError_t mix_launch(const MixTable& t, View in, View out, int64_t m, double alpha, cudaStream_t s,
-                       int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+                       int64_t r0, int64_t r1, int64_t c0, int64_t c1, int accumulate) {
   const size_t smem = sizeof(MixRow) * t.nrow + sizeof(MixTerm) * t.nterm;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(mix_kernel<VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -172,7 +179,7 @@ cudaError_t mix_launch(const MixTable& t, View in, View out, int64_t m, double a
     if (e != cudaSuccess) return e;
   }
   mix_kernel<VW><<<grid_for((r1 - r0) * ((c1 - c0 + 32 * VW - 1) / (32 * VW)), 1), 256, smem, s>>>(
-      in, out, m, t.d_table, t.nrow, t.nterm, alpha, r0, r1, c0, c1);
+      in, out, m, t.d_table, t.nrow, t.nterm, alpha, r0, r1, c0, c1, accumulate);
   return cudaGetLastError();
 }
 
@@ -194,13 +201,13 @@ static int pick_vw(int64_t m, std::initializer_list<std::pair<const void*, int64
 }
 
 static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, int64_t m,
-                                double alpha, cudaStream_t s, Rows rows) {
+                                double alpha, cudaStream_t s, Rows rows, int accumulate = 0) {
   if (t.nrow == 0) return cudaSuccess;
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   if (r1 <= r0 || c1 <= c0) return cudaSuccess;
-  if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s, r0, r1, c0, c1);
-  if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s, r0, r1, c0, c1);
-  return mix_launch<1>(t, in, out, m, alpha, s, r0, r1, c0, c1);
+  if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+  if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+  return mix_launch<1>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
 }
 
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
@@ -216,15 +223,16 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
 }
 
 cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
-                           double* C, int64_t ldc, cudaStream_t s, Rows rows) {
+                           double* C, int64_t ldc, cudaStream_t s, Rows rows, bool accumulate) {
   if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  if (pl.fixed_id >= 8 && &t == &pl.mixC)
+  if (pl.fixed_id >= 8 && &t == &pl.mixC && !accumulate)
     return launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
-  if (pl.fixed_id > 0 && pl.fixed_id < 8 && &t == &pl.mixC && fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
+  if (pl.fixed_id > 0 && pl.fixed_id < 8 && &t == &pl.mixC && !accumulate &&
+      fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
     return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
   return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
-                      pl.m, alpha, s, rows);
+                      pl.m, alpha, s, rows, accumulate ? 1 : 0);
 }
 
 }  // namespace mf

@@ -397,6 +397,31 @@ def run_plan(p, A, B):
     return host(p.dgemm(dev(A), dev(B)))
 
 
+@pytest.mark.parametrize("name,levels,n,g", [(SW, 2, 512, 5), ("laderman", 1, 288, 2), (SW, 3, 256, 3),
+                                             (SW, 1, 400, 1)])
+def test_bounded_workspace_batches(name, levels, n, g):
+    """NEXT-3 bounded workspace: products run in batches
+    of g whose T/S/P fit max_workspace; exact on integers, within the bound on
+    random inputs, workspace within the cap; too small a cap is reported."""
+    t = triples.get(name)
+    m = n // t.p ** levels
+    cap = 3 * g * m * m * 8
+    A, B = mf_inputs.pair("int1024", n, 28)
+    with mf.Plan(t, levels, n, max_workspace=cap) as p:
+        assert p.info()["workspace_bytes"] <= cap
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 29)
+        C = host(p.dgemm(dev(A), dev(B), alpha=0.5))
+    assert scaled(C, 0.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
+    with pytest.raises(mf.MfError) as e:
+        mf.Plan(t, levels, n, max_workspace=3 * m * m * 8 - 1)
+    assert e.value.status == mf.MF_ERR_OUT_OF_MEMORY
+    with mf.Plan(t, levels, n, max_workspace=1 << 40) as p:  # no batching needed
+        C2 = host(p.dgemm(dev(A), dev(B), alpha=0.5))
+    with mf.Plan(t, levels, n) as p:
+        assert (C2 == host(p.dgemm(dev(A), dev(B), alpha=0.5))).all()
+
+
 def test_host_buffer_entry_point():
     n = 256
     A, B = mf_inputs.pair("int1024", n, 14)
