@@ -316,8 +316,10 @@ def main():
     value = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
 
     # ---- roofline of the dominant kernel (K5 leaf), live over the timed region ----
-    my_prods = sum(1 for s in plan.products()["shard"] if s == rank)
+    shard = plan.products()["shard"]
     m = info["leaf_n"]
+    r0s, r1s = plan.shard_rows()  # this rank's row slab of the split leftover products
+    my_prods = sum(1 for s in shard if s == rank) + sum(1 for s in shard if s == -1) * (r1s - r0s) / m
     leaf_ms = phases["leaf"] / max(1, phases["calls"])
     leaf_flops = my_prods * 2.0 * m ** 3
     if a.level_by_level:  # the leaf phase holds the whole sub-recursion of each product

@@ -236,9 +236,11 @@ void free_plan(Plan* pl) {
     if (st) cudaStreamDestroy(st);
 }
 
-// Events of the current call when profiling is on (nullptr otherwise).
+// Events of the current call when profiling is on (nullptr otherwise).  At
+// most kMaxProfSets sets are kept between reads; later calls are not recorded.
+constexpr size_t kMaxProfSets = 4096;
 cudaEvent_t* prof_slot(Plan* pl) {
-  if (!pl->opt.profile) return nullptr;
+  if (!pl->opt.profile || pl->prof_used >= kMaxProfSets) return nullptr;
   if (pl->prof_used == pl->prof_events.size()) {
     std::vector<cudaEvent_t> set(6, nullptr);
     for (auto& e : set)

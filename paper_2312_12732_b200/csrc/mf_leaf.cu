@@ -35,6 +35,7 @@
 //    a product are rasterised in groups of 8 tile-rows for L2 reuse.
 #include <cuda.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -493,15 +494,18 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
            encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, 64, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (!ok) return cudaErrorInvalidValue;
     }
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[bn == 64]) {
+    // the >48 KB dynamic shared memory opt-in is per device: set it once per
+    // (device, tile width)
+    static std::atomic<uint64_t> attr_set[2];
+    const uint64_t dev_bit = 1ull << (dev & 63);
+    if (!(attr_set[bn == 64].load() & dev_bit)) {
       cudaError_t e = bn == 64
           ? cudaFuncSetAttribute(leaf_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_bytes<64>())
           : cudaFuncSetAttribute(leaf_dmma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_bytes<128>());
       if (e != cudaSuccess) return e;
-      attr_set[bn == 64] = true;
+      attr_set[bn == 64].fetch_or(dev_bit);
     }
     LeafParams prm;
     prm.m = a.m;
