@@ -433,10 +433,13 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   }
 
   // unsharded plans of a compiled-in triple use the specialised K4/K6
-  if (levels > 0 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) {
+  if (levels > 0 && RL <= 576 && !getenv("MF_MIX_GENERIC")) {
     pl->fixed_id = fixed_match(*pl);
     if (pl->fixed_id == 0) pl->fixed_id = kron_match(*pl);
   }
+  for (int32_t q : pl->my_prods) pl->mask_whole.w[q >> 6] |= 1ull << (q & 63);
+  for (int32_t q : pl->my_part) pl->mask_part.w[q >> 6] |= 1ull << (q & 63);
+  for (int i = 0; i < 9; ++i) pl->mask_all.w[i] = pl->mask_whole.w[i] | pl->mask_part.w[i];
 
   // ---- mix tables for this shard ----
   auto add_slots = [&](MixTable& t, int side, const std::vector<int32_t>& qs) {

@@ -114,8 +114,10 @@ __device__ __forceinline__ void acc_term(V<VW>& acc, const V<VW>& x) {
 // ---- K4: T slots (SIDE 0, from U) or S slots (SIDE 1, from V) ----
 template <const auto& T, int SIDE, int P, int VW, int Q, int... Ks>
 __device__ __forceinline__ void premix_one(const V<VW> (&x)[P * P], double* out, int64_t off,
-                                           int64_t mm, std::integer_sequence<int, Ks...>) {
+                                           int64_t mm, const ProdMask& mask,
+                                           std::integer_sequence<int, Ks...>) {
   if constexpr (!alias_v<T, SIDE, Q>) {
+    if (!mask.has(Q)) return;  // product computed by another shard
     V<VW> acc;
 #pragma unroll
     for (int e = 0; e < VW; ++e) acc.v[e] = -0.0;
@@ -126,68 +128,85 @@ __device__ __forceinline__ void premix_one(const V<VW> (&x)[P * P], double* out,
 
 template <const auto& T, int SIDE, int P, int VW, int... Qs>
 __device__ __forceinline__ void premix_all(const V<VW> (&x)[P * P], double* out, int64_t off,
-                                           int64_t mm, std::integer_sequence<int, Qs...>) {
-  (premix_one<T, SIDE, P, VW, Qs>(x, out, off, mm, std::make_integer_sequence<int, P * P>{}), ...);
+                                           int64_t mm, const ProdMask& mask,
+                                           std::integer_sequence<int, Qs...>) {
+  (premix_one<T, SIDE, P, VW, Qs>(x, out, off, mm, mask, std::make_integer_sequence<int, P * P>{}),
+   ...);
 }
 
 template <class Tag, int SIDE, int P, int R, int VW>
 __global__ void __launch_bounds__(256) premix_fixed(const double* __restrict__ X, int64_t ldx,
                                                     int64_t m, double* __restrict__ out,
                                                     int64_t r0, int64_t r1, int64_t c0,
-                                                    int64_t c1) {
+                                                    int64_t c1, const ProdMask mask) {
   constexpr int NB = P * P;
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = r0 + idx / vpr;
-    const int64_t c = c0 + (idx % vpr) * VW;
+  // grid-stride over (row, vector) positions, advanced without divisions
+  const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t sd = stride / vpr, sm = stride - sd * vpr;
+  int64_t rr = start / vpr, cv = start - rr * vpr;
+  (void)total;
+  for (; rr < r1 - r0; rr += sd, cv += sm, (cv >= vpr ? (cv -= vpr, ++rr) : 0)) {
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + cv * VW;
     V<VW> x[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) x[k] = ld_stream<VW>(X + ((k / P) * m + r) * ldx + (k % P) * m + c);
-    premix_all<Tag::T, SIDE, P, VW>(x, out, r * m + c, mm, std::make_integer_sequence<int, R>{});
+    premix_all<Tag::T, SIDE, P, VW>(x, out, r * m + c, mm, mask, std::make_integer_sequence<int, R>{});
   }
 }
 
 // ---- K6: C_i = alpha * sum_q W[i][q] * sign_q * P_q' ----
-template <const auto& T, int P, int VW, int Q, int... Is>
+template <const auto& T, int P, int VW, bool MASKED, int Q, int... Is>
 __device__ __forceinline__ void postmix_one(V<VW> (&acc)[P * P], const double* __restrict__ Pw,
-                                            int64_t off, int64_t mm,
+                                            int64_t off, int64_t mm, const ProdMask& mask,
                                             std::integer_sequence<int, Is...>) {
   constexpr int nz = (0 + ... + (coef_v<T, 2, Is, Q> != 0));
   if constexpr (nz > 0) {
+    if constexpr (MASKED)
+      if (!mask.has(Q)) return;  // product of another shard
     const V<VW> x = ld_stream<VW>(Pw + (int64_t)Q * mm + off);
     (acc_term<coef_v<T, 2, Is, Q> * sign_v<T, Q>, VW>(acc[Is], x), ...);
   }
 }
 
-template <const auto& T, int P, int VW, int... Qs>
+template <const auto& T, int P, int VW, bool MASKED, int... Qs>
 __device__ __forceinline__ void postmix_all(V<VW> (&acc)[P * P], const double* __restrict__ Pw,
-                                            int64_t off, int64_t mm,
+                                            int64_t off, int64_t mm, const ProdMask& mask,
                                             std::integer_sequence<int, Qs...>) {
-  (postmix_one<T, P, VW, Qs>(acc, Pw, off, mm, std::make_integer_sequence<int, P * P>{}), ...);
+  (postmix_one<T, P, VW, MASKED, Qs>(acc, Pw, off, mm, mask,
+                                     std::make_integer_sequence<int, P * P>{}),
+   ...);
 }
 
-template <class Tag, int P, int R, int VW>
+template <class Tag, int P, int R, int VW, bool MASKED>
 __global__ void __launch_bounds__(256) postmix_fixed(const double* __restrict__ Pw, int64_t m,
                                                      double alpha, double* __restrict__ C,
                                                      int64_t ldc, int64_t r0, int64_t r1,
-                                                     int64_t c0, int64_t c1) {
+                                                     int64_t c0, int64_t c1, const ProdMask mask) {
   constexpr int NB = P * P;
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = r0 + idx / vpr;
-    const int64_t c = c0 + (idx % vpr) * VW;
+  // grid-stride over (row, vector) positions, advanced without divisions
+  const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t sd = stride / vpr, sm = stride - sd * vpr;
+  int64_t rr = start / vpr, cv = start - rr * vpr;
+  (void)total;
+  for (; rr < r1 - r0; rr += sd, cv += sm, (cv >= vpr ? (cv -= vpr, ++rr) : 0)) {
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + cv * VW;
     V<VW> acc[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i)
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc[i].v[e] = -0.0;
-    postmix_all<Tag::T, P, VW>(acc, Pw, r * m + c, mm, std::make_integer_sequence<int, R>{});
+    postmix_all<Tag::T, P, VW, MASKED>(acc, Pw, r * m + c, mm, mask,
+                                       std::make_integer_sequence<int, R>{});
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       if (alpha != 1.0) {
@@ -221,20 +240,29 @@ bool equal(const Tri<NB, R>& t, const Plan& pl) {
 
 template <class Tag, int P, int R, int VW>
 cudaError_t run_premix(int side, const double* X, int64_t ldx, int64_t m, double* out,
-                       cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+                       cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                       const ProdMask& mask) {
   const int grid = grid_for((r1 - r0) * ((c1 - c0) / VW));
   if (side == 0)
-    premix_fixed<Tag, 0, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1);
+    premix_fixed<Tag, 0, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1, mask);
   else
-    premix_fixed<Tag, 1, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1);
+    premix_fixed<Tag, 1, P, R, VW><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1, mask);
   return cudaGetLastError();
 }
 
 template <class Tag, int P, int R, int VW>
 cudaError_t run_postmix(const double* Pw, int64_t m, double alpha, double* C, int64_t ldc,
-                        cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
-  postmix_fixed<Tag, P, R, VW><<<grid_for((r1 - r0) * ((c1 - c0) / VW)), 256, 0, s>>>(
-      Pw, m, alpha, C, ldc, r0, r1, c0, c1);
+                        cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                        const ProdMask& mask) {
+  // the unmasked instantiation keeps every product's load free to be hoisted
+  bool full = true;
+  for (int q = 0; q < R; ++q) full = full && mask.has(q);
+  if (full)
+    postmix_fixed<Tag, P, R, VW, false><<<grid_for((r1 - r0) * ((c1 - c0) / VW)), 256, 0, s>>>(
+        Pw, m, alpha, C, ldc, r0, r1, c0, c1, mask);
+  else
+    postmix_fixed<Tag, P, R, VW, true><<<grid_for((r1 - r0) * ((c1 - c0) / VW)), 256, 0, s>>>(
+        Pw, m, alpha, C, ldc, r0, r1, c0, c1, mask);
   return cudaGetLastError();
 }
 
@@ -275,18 +303,19 @@ bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t 
 }
 
 cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
-                                double* out, cudaStream_t s, Rows rows) {
+                                double* out, cudaStream_t s, Rows rows, const ProdMask& mask) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
-#define PRE(T_, P_, R_) fixed::run_premix<T_, P_, R_, 4>(side, X, ldx, m, out, s, r0, r1, c0, c1)
+#define PRE(T_, P_, R_) \
+  fixed::run_premix<T_, P_, R_, 4>(side, X, ldx, m, out, s, r0, r1, c0, c1, mask)
   MF_FIXED_SWITCH(id, PRE)
 #undef PRE
 }
 
 cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
-                                 int64_t ldc, cudaStream_t s, Rows rows) {
+                                 int64_t ldc, cudaStream_t s, Rows rows, const ProdMask& mask) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
 #define POST(T_, P_, R_) \
-  fixed::run_postmix<T_, P_, R_, (P_ >= 4 ? 2 : 4)>(Pw, m, alpha, C, ldc, s, r0, r1, c0, c1)
+  fixed::run_postmix<T_, P_, R_, (P_ >= 4 ? 2 : 4)>(Pw, m, alpha, C, ldc, s, r0, r1, c0, c1, mask)
   MF_FIXED_SWITCH(id, POST)
 #undef POST
 }

@@ -28,6 +28,13 @@ struct Product {
   int32_t shard;         // shard that computes it
 };
 
+// Product mask for the specialised K4/K6 (bit q = product q is computed by
+// this plan's shard; up to 576 products).  Passed by value to the kernels.
+struct ProdMask {
+  uint64_t w[9];
+  __host__ __device__ bool has(int q) const { return (w[q >> 6] >> (q & 63)) & 1ull; }
+};
+
 // Device-side routing entry of the leaf kernel (kept POD, 16 bytes).
 struct LeafJob {
   int32_t a_coord;  // SRC_INPUT: (block_row << 16) | block_col; SRC_WORKSPACE: slot
@@ -86,6 +93,7 @@ struct Plan {
   MixTable mixC;                  // post-addition over the whole products (zero coef elsewhere)
   MixTable mixC2;                 // ... plus the split products (used on rows part_rows)
   int n_jobs_part = 0;            // leaf jobs of split products follow the whole ones in d_jobs
+  ProdMask mask_whole{}, mask_part{}, mask_all{};  // for the specialised K4/K6
   // bounded workspace (mf_options.max_workspace): product batches with local
   // slot numbering; each has its own K4/K6 tables and leaf jobs (d_jobs + job0)
   struct Batch {
@@ -156,15 +164,15 @@ bool leaf_tma_supported(const LeafArgs& a);
 int fixed_match(const Plan& pl);
 bool fixed_vw4_ok(int64_t m, const void* a, int64_t lda, const void* b, int64_t ldb);
 cudaError_t launch_premix_fixed(int id, int side, const double* X, int64_t ldx, int64_t m,
-                                double* out, cudaStream_t s, Rows rows);
+                                double* out, cudaStream_t s, Rows rows, const ProdMask& mask);
 cudaError_t launch_postmix_fixed(int id, const double* Pw, int64_t m, double alpha, double* C,
-                                 int64_t ldc, cudaStream_t s, Rows rows);
+                                 int64_t ldc, cudaStream_t s, Rows rows, const ProdMask& mask);
 // mf_kron.cu: Kronecker-factored K4/K6 for deep powers (ids >= 8)
 int kron_match(const Plan& pl);
 cudaError_t launch_premix_kron(int id, int side, const double* X, int64_t ldx, int64_t m,
-                               double* out, cudaStream_t s, Rows rows);
+                               double* out, cudaStream_t s, Rows rows, const ProdMask& mask);
 cudaError_t launch_postmix_kron(int id, const double* Pw, int64_t m, double alpha, double* C,
-                                int64_t ldc, cudaStream_t s, Rows rows);
+                                int64_t ldc, cudaStream_t s, Rows rows, const ProdMask& mask);
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s);
 
 }  // namespace mf

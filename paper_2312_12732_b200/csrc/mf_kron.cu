@@ -190,23 +190,25 @@ __device__ __forceinline__ void st1(double* p, const V<VW>& x) {
 // in[] holds NB_from(LEV) values indexed (k_LEV, k_LEV+1..k_L-1).
 template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
 __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64_t off, int64_t mm,
-                                      std::integer_sequence<int, Ks...>);
+                                      const ProdMask& mask, std::integer_sequence<int, Ks...>);
 
 template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int... Qs>
 __device__ __forceinline__ void pre_stage(const V<VW> (&in)[NIN], double* out, int64_t off,
-                                          int64_t mm, std::integer_sequence<int, Qs...>) {
-  (pre_q<Ch, SIDE, VW, LEV, QP, NIN, Qs>(in, out, off, mm,
+                                          int64_t mm, const ProdMask& mask,
+                                          std::integer_sequence<int, Qs...>) {
+  (pre_q<Ch, SIDE, VW, LEV, QP, NIN, Qs>(in, out, off, mm, mask,
                                          std::make_integer_sequence<int, Ch::NB(LEV)>{}),
    ...);
 }
 
 template <class Ch, int SIDE, int VW, int LEV, int QP, int NIN, int Q, int... Ks>
 __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64_t off, int64_t mm,
-                                      std::integer_sequence<int, Ks...>) {
+                                      const ProdMask& mask, std::integer_sequence<int, Ks...>) {
   constexpr int NOUT = NIN / Ch::NB(LEV);
   constexpr int q = QP * Ch::R_of(LEV) + Q;
   if constexpr (LEV == Ch::L - 1) {
     if constexpr (slot_v<Ch, SIDE, q> >= 0) {
+      if (!mask.has(q)) return;  // product of another shard
       V<VW> y;
 #pragma unroll
       for (int e = 0; e < VW; ++e) y.v[e] = -0.0;
@@ -221,7 +223,7 @@ __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64
       for (int e = 0; e < VW; ++e) y[kk].v[e] = -0.0;
       (acc_term<coef<Ch, LEV, SIDE, Ks, Q>, VW>(y[kk], in[Ks * NOUT + kk]), ...);
     }
-    pre_stage<Ch, SIDE, VW, LEV + 1, q, NOUT>(y, out, off, mm,
+    pre_stage<Ch, SIDE, VW, LEV + 1, q, NOUT>(y, out, off, mm, mask,
                                               std::make_integer_sequence<int, Ch::R_of(LEV + 1)>{});
   }
 }
@@ -229,24 +231,30 @@ __device__ __forceinline__ void pre_q(const V<VW> (&in)[NIN], double* out, int64
 template <class Ch, int SIDE, int VW>
 __global__ void __launch_bounds__(256) premix_kron(const double* __restrict__ X, int64_t ldx,
                                                    int64_t m, double* __restrict__ out, int64_t r0,
-                                                   int64_t r1, int64_t c0, int64_t c1) {
+                                                   int64_t r1, int64_t c0, int64_t c1,
+                                                   const ProdMask mask) {
   static_assert(unsigned_aliases<Ch>, "sign folding not supported on this path");
   constexpr int NB = Ch::NB_from(0);
   constexpr int P = Ch::P();
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = r0 + idx / vpr;
-    const int64_t c = c0 + (idx % vpr) * VW;
+  // grid-stride over (row, vector) positions, advanced without divisions
+  const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t sd = stride / vpr, sm = stride - sd * vpr;
+  int64_t rr = start / vpr, cv = start - rr * vpr;
+  (void)total;
+  for (; rr < r1 - r0; rr += sd, cv += sm, (cv >= vpr ? (cv -= vpr, ++rr) : 0)) {
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + cv * VW;
     V<VW> x[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) {
       const int b = flat_block<Ch>(k);
       x[k] = ld1<VW>(X + ((b / P) * m + r) * ldx + (b % P) * m + c);
     }
-    pre_stage<Ch, SIDE, VW, 0, 0, NB>(x, out, r * m + c, mm,
+    pre_stage<Ch, SIDE, VW, 0, 0, NB>(x, out, r * m + c, mm, mask,
                                       std::make_integer_sequence<int, Ch::R_of(0)>{});
   }
 }
@@ -256,26 +264,31 @@ __global__ void __launch_bounds__(256) premix_kron(const double* __restrict__ X,
 // partial C values indexed (i_LEV, i_LEV+1..); the deepest level combines leaf
 // products over its q, each shallower level combines the level below (inner
 // first, as the recursion distributes P_i).
-template <class Ch, int VW, int LEV, int QP, int NACC, int Q, int... Is>
+template <class Ch, int VW, bool MASKED, int LEV, int QP, int NACC, int Q, int... Is>
 __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
-                                       int64_t off, int64_t mm, std::integer_sequence<int, Is...>);
+                                       int64_t off, int64_t mm, const ProdMask& mask,
+                                       std::integer_sequence<int, Is...>);
 
-template <class Ch, int VW, int LEV, int QP, int NACC, int... Qs>
+template <class Ch, int VW, bool MASKED, int LEV, int QP, int NACC, int... Qs>
 __device__ __forceinline__ void post_stage(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
-                                           int64_t off, int64_t mm,
+                                           int64_t off, int64_t mm, const ProdMask& mask,
                                            std::integer_sequence<int, Qs...>) {
-  (post_q<Ch, VW, LEV, QP, NACC, Qs>(acc, Pw, off, mm, std::make_integer_sequence<int, Ch::NB(LEV)>{}),
+  (post_q<Ch, VW, MASKED, LEV, QP, NACC, Qs>(acc, Pw, off, mm, mask,
+                                     std::make_integer_sequence<int, Ch::NB(LEV)>{}),
    ...);
 }
 
-template <class Ch, int VW, int LEV, int QP, int NACC, int Q, int... Is>
+template <class Ch, int VW, bool MASKED, int LEV, int QP, int NACC, int Q, int... Is>
 __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restrict__ Pw,
-                                       int64_t off, int64_t mm, std::integer_sequence<int, Is...>) {
+                                       int64_t off, int64_t mm, const ProdMask& mask,
+                                       std::integer_sequence<int, Is...>) {
   constexpr int NSUB = NACC / Ch::NB(LEV);
   constexpr int q = QP * Ch::R_of(LEV) + Q;
   constexpr int nz = (0 + ... + (coef<Ch, LEV, 2, Is, Q> != 0));
   if constexpr (nz > 0) {
     if constexpr (LEV == Ch::L - 1) {
+      if constexpr (MASKED)
+        if (!mask.has(q)) return;  // product of another shard
       const V<VW> x = ld1<VW>(Pw + (int64_t)q * mm + off);
       (acc_term<coef<Ch, LEV, 2, Is, Q>, VW>(acc[Is], x), ...);
     } else {
@@ -284,7 +297,7 @@ __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restr
       for (int rr = 0; rr < NSUB; ++rr)
 #pragma unroll
         for (int e = 0; e < VW; ++e) y[rr].v[e] = -0.0;
-      post_stage<Ch, VW, LEV + 1, q, NSUB>(y, Pw, off, mm,
+      post_stage<Ch, VW, MASKED, LEV + 1, q, NSUB>(y, Pw, off, mm, mask,
                                            std::make_integer_sequence<int, Ch::R_of(LEV + 1)>{});
 #pragma unroll
       for (int rr = 0; rr < NSUB; ++rr)
@@ -293,27 +306,32 @@ __device__ __forceinline__ void post_q(V<VW> (&acc)[NACC], const double* __restr
   }
 }
 
-template <class Ch, int VW>
+template <class Ch, int VW, bool MASKED>
 __global__ void __launch_bounds__(256) postmix_kron(const double* __restrict__ Pw, int64_t m,
                                                     double alpha, double* __restrict__ C,
                                                     int64_t ldc, int64_t r0, int64_t r1, int64_t c0,
-                                                    int64_t c1) {
+                                                    int64_t c1, const ProdMask mask) {
   static_assert(unsigned_aliases<Ch>, "sign folding not supported on this path");
   constexpr int NB = Ch::NB_from(0);
   constexpr int P = Ch::P();
   const int64_t vpr = (c1 - c0) / VW;
   const int64_t total = (r1 - r0) * vpr;
   const int64_t mm = m * m;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = r0 + idx / vpr;
-    const int64_t c = c0 + (idx % vpr) * VW;
+  // grid-stride over (row, vector) positions, advanced without divisions
+  const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t sd = stride / vpr, sm = stride - sd * vpr;
+  int64_t rr = start / vpr, cv = start - rr * vpr;
+  (void)total;
+  for (; rr < r1 - r0; rr += sd, cv += sm, (cv >= vpr ? (cv -= vpr, ++rr) : 0)) {
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + cv * VW;
     V<VW> acc[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i)
 #pragma unroll
       for (int e = 0; e < VW; ++e) acc[i].v[e] = -0.0;
-    post_stage<Ch, VW, 0, 0, NB>(acc, Pw, r * m + c, mm,
+    post_stage<Ch, VW, MASKED, 0, 0, NB>(acc, Pw, r * m + c, mm, mask,
                                  std::make_integer_sequence<int, Ch::R_of(0)>{});
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -406,25 +424,40 @@ int kron_match(const Plan& pl) {
     default: return cudaErrorInvalidValue;   \
   }
 
+// number of products of chain id (for the mask-is-full test)
+static int pl_products(int id) {
+  switch (id) {
+    case 8: case 9: case 10: return 343;
+    case 11: return 529;
+    case 12: case 13: return 161;
+    default: return 0;
+  }
+}
+
 cudaError_t launch_premix_kron(int id, int side, const double* X, int64_t ldx, int64_t m,
-                               double* out, cudaStream_t s, Rows rows) {
+                               double* out, cudaStream_t s, Rows rows, const ProdMask& mask) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   const int grid = kronmix::grid_for((r1 - r0) * (c1 - c0));
 #define PRE(CH_)                                                                                  \
-  (side == 0 ? (kronmix::premix_kron<CH_, 0, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
+  (side == 0 ? (kronmix::premix_kron<CH_, 0, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1, mask), \
                 cudaGetLastError())                                                               \
-             : (kronmix::premix_kron<CH_, 1, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1), \
+             : (kronmix::premix_kron<CH_, 1, 1><<<grid, 256, 0, s>>>(X, ldx, m, out, r0, r1, c0, c1, mask), \
                 cudaGetLastError()))
   MF_KRON_SWITCH(id, PRE)
 #undef PRE
 }
 
 cudaError_t launch_postmix_kron(int id, const double* Pw, int64_t m, double alpha, double* C,
-                                int64_t ldc, cudaStream_t s, Rows rows) {
+                                int64_t ldc, cudaStream_t s, Rows rows, const ProdMask& mask) {
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   const int grid = kronmix::grid_for((r1 - r0) * (c1 - c0));
-#define POST(CH_)                                                                              \
-  (kronmix::postmix_kron<CH_, 1><<<grid, 256, 0, s>>>(Pw, m, alpha, C, ldc, r0, r1, c0, c1), \
+  bool full = true;
+  for (int q = 0; q < 576; ++q) full = full && (q >= pl_products(id) || mask.has(q));
+#define POST(CH_)                                                                                 \
+  (full ? kronmix::postmix_kron<CH_, 1, false><<<grid, 256, 0, s>>>(Pw, m, alpha, C, ldc, r0, r1, c0, \
+                                                                    c1, mask)                      \
+        : kronmix::postmix_kron<CH_, 1, true><<<grid, 256, 0, s>>>(Pw, m, alpha, C, ldc, r0, r1, c0,  \
+                                                                   c1, mask),                      \
    cudaGetLastError())
   MF_KRON_SWITCH(id, POST)
 #undef POST

@@ -121,8 +121,9 @@ __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
   const int64_t segs_per_row = (c1 - c0 + SEG - 1) / SEG;
   const int64_t total = (r1 - r0) * segs_per_row;
   for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
-    const int64_t r = r0 + seg / segs_per_row;
-    const int64_t c = c0 + (seg % segs_per_row) * SEG + lane * VW;
+    const int64_t rr = seg / segs_per_row;
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + (seg - rr * segs_per_row) * SEG + lane * VW;
     if (c >= c1) continue;
     for (int o = warp; o < nrow; o += 8) {
       const MixRow row = rows[o];
@@ -213,10 +214,16 @@ static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, in
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows) {
   if (t.nrow == 0 || rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  if (pl.fixed_id >= 8)
-    return launch_premix_kron(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s, rows);
-  if (pl.fixed_id > 0 && fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
-    return launch_premix_fixed(pl.fixed_id, &t == &pl.mixA ? 0 : 1, X, ldx, pl.m, out, s, rows);
+  // specialised kernels serve the plan's own tables; the shard's product mask
+  // selects the outputs (A: whole products, or split products on their rows)
+  const bool own = &t == &pl.mixA || &t == &pl.mixA2 || &t == &pl.mixB;
+  if (pl.fixed_id > 0 && own) {
+    const int side = &t == &pl.mixB ? 1 : 0;
+    const ProdMask& mask = &t == &pl.mixA ? pl.mask_whole : (&t == &pl.mixA2 ? pl.mask_part : pl.mask_all);
+    if (pl.fixed_id >= 8) return launch_premix_kron(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
+    if (fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
+      return launch_premix_fixed(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
+  }
   const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
   return mix_dispatch(vw, t, View{const_cast<double*>(X), ldx, pl.P}, View{out, pl.m, 0}, pl.m,
                       1.0, s, rows);
@@ -225,11 +232,12 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
 cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
                            double* C, int64_t ldc, cudaStream_t s, Rows rows, bool accumulate) {
   if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  if (pl.fixed_id >= 8 && &t == &pl.mixC && !accumulate)
-    return launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
-  if (pl.fixed_id > 0 && pl.fixed_id < 8 && &t == &pl.mixC && !accumulate &&
-      fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
-    return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows);
+  if (pl.fixed_id > 0 && !accumulate && (&t == &pl.mixC || &t == &pl.mixC2)) {
+    const ProdMask& mask = &t == &pl.mixC ? pl.mask_whole : pl.mask_all;
+    if (pl.fixed_id >= 8) return launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
+    if (fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
+      return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
+  }
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
   return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
                       pl.m, alpha, s, rows, accumulate ? 1 : 0);
