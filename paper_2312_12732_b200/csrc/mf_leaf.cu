@@ -45,27 +45,34 @@
 namespace mf {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;  // BN: the default (widest) tile
-constexpr int STAGES = 5;
+constexpr int BM = 128, BN = 128, BK = 16;  // BN: the default (widest) tile; BK: one k sub-block
 constexpr int MMA_WARPS = 8;
 constexpr int THREADS = MMA_WARPS * 32;
-constexpr int A_BYTES = BM * BK * 8;
-template <int BNT> __host__ __device__ constexpr int stage_bytes() { return A_BYTES + BK * BNT * 8; }
-template <int BNT> __host__ __device__ constexpr int smem_bytes() { return STAGES * stage_bytes<BNT>() + 2 * STAGES * 8 + 1024; }
+constexpr int A_SUB_BYTES = BM * BK * 8;  // one [128 m][16 k] swizzled A sub-tile
+// A stage holds KSUB k sub-blocks (16 k each): A as KSUB swizzled sub-tiles,
+// B as one [16*KSUB k][BNT n] box.  Deeper stages (KSUB = 2) halve the
+// mbarrier waits per flop; the ring depth keeps ~190 KB of smem in flight.
+template <int BNT, int KSUB> __host__ __device__ constexpr int a_bytes() { return KSUB * A_SUB_BYTES; }
+template <int BNT, int KSUB> __host__ __device__ constexpr int stage_bytes() {
+  return KSUB * A_SUB_BYTES + KSUB * BK * BNT * 8;
+}
+template <int BNT, int KSUB> __host__ __device__ constexpr int n_stages() {
+  return (192 * 1024) / stage_bytes<BNT, KSUB>() < 5 ? (192 * 1024) / stage_bytes<BNT, KSUB>() : 5;
+}
+template <int BNT, int KSUB> __host__ __device__ constexpr int smem_bytes() {
+  return n_stages<BNT, KSUB>() * stage_bytes<BNT, KSUB>() + 2 * n_stages<BNT, KSUB>() * 8 + 1024;
+}
 constexpr int GROUP_M = 8;
 
-// B-tile staging modes (all TMA):
-//   B_ROWS:  one box [16 k][128 n], no swizzle (1 KB rows; LDS.128 4-way conflicted)
-//   B_BOXES: 8 boxes [16 k][16 n], SWIZZLE_128B (conflict-free, 8 TMA issues)
-//   B_5D:    one 5-D box {16 n, 16 k, 8 n-blocks} giving the B_BOXES layout with
-//            one TMA issue (needs m % 16 == 0)
-enum BMode : int { B_ROWS = 0, B_BOXES = 1, B_5D = 2 };
+// B staging: one unswizzled TMA box [16*KSUB k][BNT n] per stage.  Its LDS.128
+// are 4-way bank conflicted; the conflict-free swizzled alternatives (8 boxes
+// of [16 k][16 n], or one 5-D box with that layout) measured slower or equal
+// (profiles/leaf_bmode_r01.json: TMA issues per stage, not smem banks, limit).
 
 struct LeafParams {
   int64_t m;
   int tm0, tn0;  // first tile row / column (region of the host-buffer pipeline)
-  int tiles_m, tiles_n, kblocks;
-  int bmode;
+  int tiles_m, tiles_n, kblocks;  // kblocks: stages of 16*KSUB k
   double* out;
   int64_t ldo, out_stride;
   double alpha;
@@ -119,16 +126,6 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                            int c0, int c1, int c2, int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
-      :: "r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-         "r"(c4), "r"(bar)
-      : "memory");
-}
-
 __device__ __forceinline__ void lds128(uint32_t addr, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
 }
@@ -141,13 +138,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // BNT = CTA tile width (128, or 64 to cut wave quantisation on small batches):
 // warps form a 2 x 4 grid of 64 x (BNT/4) warp tiles, NJ = BNT/64 16-column
 // groups per warp.
-template <int BNT>
+template <int BNT, int KSUB>
 __global__ void __launch_bounds__(THREADS, 1)
 leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
                  const LeafParams prm) {
   constexpr int NJ = BNT / 64, WN = BNT / 4;
-  constexpr int STAGE_BYTES = stage_bytes<BNT>();
+  constexpr int STAGES = n_stages<BNT, KSUB>();
+  constexpr int STAGE_BYTES = stage_bytes<BNT, KSUB>();
+  constexpr int A_BYTES = a_bytes<BNT, KSUB>();
+  constexpr int KS = BK * KSUB;  // k per stage
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -189,21 +189,13 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t fb = full0 + 8 * s;
     mbar_expect_tx(fb, STAGE_BYTES);
     const uint32_t dA = s_base + s * STAGE_BYTES, dB = dA + A_BYTES;
-    if (a_ws) tma_load_3d(dA, mapA, fb, kb * BK, tm * BM, job.a_coord);
-    else      tma_load_4d(dA, mapA, fb, kb * BK, a_bc, tm * BM, a_br);
-    if (prm.bmode == B_BOXES) {
 #pragma unroll
-      for (int j = 0; j < BNT / 16; ++j) {
-        if (b_ws) tma_load_3d(dB + j * 2048, mapB, fb, tn * BNT + 16 * j, kb * BK, job.b_coord);
-        else      tma_load_4d(dB + j * 2048, mapB, fb, tn * BNT + 16 * j, b_bc, kb * BK, b_br);
-      }
-    } else if (prm.bmode == B_5D) {
-      if (b_ws) tma_load_4d(dB, mapB, fb, 0, kb * BK, tn * (BNT / 16), job.b_coord);
-      else      tma_load_5d(dB, mapB, fb, 0, kb * BK, tn * (BNT / 16), b_bc, b_br);
-    } else {
-      if (b_ws) tma_load_3d(dB, mapB, fb, tn * BNT, kb * BK, job.b_coord);
-      else      tma_load_4d(dB, mapB, fb, tn * BNT, b_bc, kb * BK, b_br);
+    for (int j = 0; j < KSUB; ++j) {
+      if (a_ws) tma_load_3d(dA + j * A_SUB_BYTES, mapA, fb, kb * KS + j * BK, tm * BM, job.a_coord);
+      else      tma_load_4d(dA + j * A_SUB_BYTES, mapA, fb, kb * KS + j * BK, a_bc, tm * BM, a_br);
     }
+    if (b_ws) tma_load_3d(dB, mapB, fb, tn * BNT, kb * KS, job.b_coord);
+    else      tma_load_4d(dB, mapB, fb, tn * BNT, b_bc, kb * KS, b_br);
   };
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapA)) : "memory");
@@ -231,33 +223,29 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint32_t offA[2], offB[2][2];
   offA[0] = (wm * 64 + lr) * 128 + ((c0 ^ lr) << 4);
   offA[1] = (wm * 64 + lr) * 128 + ((c1 ^ lr) << 4);
-  uint32_t nj_stride;
 #pragma unroll
   for (int s2 = 0; s2 < 2; ++s2) {
     const uint32_t r0 = 2 * c0 + s2, r1 = 2 * c1 + s2;  // B rows (k) for g = 0, 1
-    if (prm.bmode == B_ROWS) {
-      offB[0][s2] = r0 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
-      offB[1][s2] = r1 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
-    } else {
-      offB[0][s2] = (NJ * wn) * 2048 + r0 * 128 + ((lr ^ (r0 & 7)) << 4);
-      offB[1][s2] = (NJ * wn) * 2048 + r1 * 128 + ((lr ^ (r1 & 7)) << 4);
-    }
+    offB[0][s2] = r0 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
+    offB[1][s2] = r1 * (BNT * 8) + (wn * WN + 2 * lr) * 8;
   }
-  nj_stride = prm.bmode == B_ROWS ? 16 * 8 : 2048;
 
   // Fragment double buffering: group g+1's LDS are issued before group g's 64
   // DMMAs, so no k-group starts on an LDS-latency bubble.  A stage's slot is
   // released (mbarrier.arrive has release semantics: the LDS reads are
-  // complete) as soon as its last fragment load has been issued.
+  // complete) as soon as its last fragment load has been issued.  Group g of
+  // a stage = k sub-block g/2, half g%2 (8 k each).
   double fa0[8][2], fb0[NJ][2][2], fa1[8][2], fb1[NJ][2][2];
   auto load_frags = [&](uint32_t sA, uint32_t sB, int g, double (&fa)[8][2], double (&fb)[NJ][2][2]) {
+    const uint32_t a = sA + (g >> 1) * A_SUB_BYTES + offA[g & 1];
+    const uint32_t b = sB + (g >> 1) * (BK * BNT * 8) + 0;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) lds128(sA + offA[g] + mi * 8 * 128, fa[mi][0], fa[mi][1]);
+    for (int mi = 0; mi < 8; ++mi) lds128(a + mi * 8 * 128, fa[mi][0], fa[mi][1]);
 #pragma unroll
     for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
       for (int s2 = 0; s2 < 2; ++s2)
-        lds128(sB + offB[g][s2] + nj * nj_stride, fb[nj][s2][0], fb[nj][s2][1]);
+        lds128(b + offB[g & 1][s2] + nj * 16 * 8, fb[nj][s2][0], fb[nj][s2][1]);
   };
   auto mma_group = [&](const double (&fa)[8][2], const double (&fb)[NJ][2][2]) {
 #pragma unroll
@@ -285,17 +273,24 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
     const int s = kb % STAGES;
     const uint32_t sA = s_base + s * STAGE_BYTES, sB = sA + A_BYTES;
-    load_frags(sA, sB, 1, fa1, fb1);  // group 1 of this stage
-    mma_group(fa0, fb0);              // group 0 of this stage
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * s);
-    if (kb + 1 < prm.kblocks) {       // group 0 of the next stage
-      const int s1 = (kb + 1) % STAGES;
-      mbar_wait(full0 + 8 * s1, ((kb + 1) / STAGES) & 1);
-      const uint32_t nA = s_base + s1 * STAGE_BYTES;
-      load_frags(nA, nA + A_BYTES, 0, fa0, fb0);
+#pragma unroll
+    for (int gg = 0; gg < 2 * KSUB; gg += 2) {
+      load_frags(sA, sB, gg + 1, fa1, fb1);  // group gg+1 of this stage
+      mma_group(fa0, fb0);                   // group gg
+      if (gg + 2 < 2 * KSUB) {
+        load_frags(sA, sB, gg + 2, fa0, fb0);
+      } else {                               // last group: release, prefetch next stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * s);
+        if (kb + 1 < prm.kblocks) {
+          const int s1 = (kb + 1) % STAGES;
+          mbar_wait(full0 + 8 * s1, ((kb + 1) / STAGES) & 1);
+          const uint32_t nA = s_base + s1 * STAGE_BYTES;
+          load_frags(nA, nA + A_BYTES, 0, fa0, fb0);
+        }
+      }
+      mma_group(fa1, fb1);                   // group gg+1
     }
-    mma_group(fa1, fb1);              // group 1 of this stage
   }
 
   // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
@@ -407,31 +402,6 @@ bool encode_slot_view(CUtensorMap* map, const double* X, int slots, int64_t m, u
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 5-D view of B for B_5D: {n-in-16, row, n-block-of-16, block-col, block-row}
-// (or 4-D {n-in-16, row, n-block, slot} for a workspace); box {16, 16, 8, 1, 1}
-// lands in shared memory as 8 consecutive [16 k][16 n] sub-tiles.
-bool encode_b5d(CUtensorMap* map, const double* X, int64_t ld, int P, int64_t m, bool slots,
-                int n_slots) {
-  if (slots) {
-    cuuint64_t dims[4] = {16, (cuuint64_t)m, (cuuint64_t)(m / 16), (cuuint64_t)(n_slots > 0 ? n_slots : 1)};
-    cuuint64_t strides[3] = {(cuuint64_t)m * 8, 128, (cuuint64_t)m * m * 8};
-    cuuint32_t box[4] = {16, 16, 8, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims,
-                       strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-           CUDA_SUCCESS;
-  }
-  cuuint64_t dims[5] = {16, (cuuint64_t)m, (cuuint64_t)(m / 16), (cuuint64_t)P, (cuuint64_t)P};
-  cuuint64_t strides[4] = {(cuuint64_t)ld * 8, 128, (cuuint64_t)m * 8, (cuuint64_t)m * ld * 8};
-  cuuint32_t box[5] = {16, 16, 8, 1, 1};
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  return encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(X), dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
-
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -450,32 +420,6 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cudaSuccess;
   if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && r0 % BM == 0 && c0 % BN == 0 &&
       (c1 == a.m || c1 % BN == 0)) {
-    int bmode = B_ROWS;  // measured fastest (profiles/leaf_bmode_r01.json)
-    if (const char* e = getenv("MF_LEAF_BMODE")) bmode = atoi(e);  // experiments: 0, 1, 2
-    if (bmode == B_5D && a.m % 16 != 0) bmode = B_BOXES;
-    CUtensorMap mA, mT, mB, mS;
-    bool ok = encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-              encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM,
-                               CU_TENSOR_MAP_SWIZZLE_128B);
-    if (bmode == B_5D) {
-      ok = ok && encode_b5d(&mB, a.B, a.ldb, a.P, a.m, false, 0) &&
-           encode_b5d(&mS, a.S ? a.S : a.B, a.m, 1, a.m, true, a.n_slots_b);
-      if (!ok) {  // fall back to per-sub-tile boxes if the 5-D view is rejected
-        bmode = B_BOXES;
-        ok = encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-             encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM,
-                              CU_TENSOR_MAP_SWIZZLE_128B);
-      }
-    }
-    if (bmode == B_BOXES)
-      ok = ok && encode_block_view(&mB, a.B, a.ldb, a.P, a.m, 16, BK, CU_TENSOR_MAP_SWIZZLE_128B) &&
-           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, 16, BK,
-                            CU_TENSOR_MAP_SWIZZLE_128B);
-    if (bmode == B_ROWS)
-      ok = ok && encode_block_view(&mB, a.B, a.ldb, a.P, a.m, BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, BN, BK,
-                            CU_TENSOR_MAP_SWIZZLE_NONE);
-    if (!ok) return cudaErrorInvalidValue;
     // Tile width: 64 when 128-wide tiles would leave a badly filled last wave
     // (e.g. 7 products of 2048^2: 12.1 waves of 148 SMs) -- model: wave fill
     // times a 2% per-tile penalty for the narrower tile (MF_LEAF_BN overrides).
@@ -487,34 +431,24 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
       const double waves = (double)(tm_tiles * ((c1 - c0 + bn - 1) / bn) * a.n_jobs) / sms;
       return waves / std::ceil(waves);
     };
-    int bn = (bmode == B_ROWS && fill(64) * 0.98 > fill(128)) ? 64 : 128;
-    if (const char* e = getenv("MF_LEAF_BN")) bn = atoi(e) == 64 && bmode == B_ROWS ? 64 : 128;
-    if (bn == 64) {  // re-encode B with 64-wide boxes
-      ok = encode_block_view(&mB, a.B, a.ldb, a.P, a.m, 64, BK, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-           encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, 64, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
-      if (!ok) return cudaErrorInvalidValue;
-    }
-    // the >48 KB dynamic shared memory opt-in is per device: set it once per
-    // (device, tile width)
-    static std::atomic<uint64_t> attr_set[2];
-    const uint64_t dev_bit = 1ull << (dev & 63);
-    if (!(attr_set[bn == 64].load() & dev_bit)) {
-      cudaError_t e = bn == 64
-          ? cudaFuncSetAttribute(leaf_dmma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes<64>())
-          : cudaFuncSetAttribute(leaf_dmma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes<128>());
-      if (e != cudaSuccess) return e;
-      attr_set[bn == 64].fetch_or(dev_bit);
-    }
+    int bn = fill(64) * 0.98 > fill(128) ? 64 : 128;
+    if (const char* e = getenv("MF_LEAF_BN")) bn = atoi(e) == 64 ? 64 : 128;
+    int ksub = 2;  // k sub-blocks of 16 per pipeline stage
+    if (const char* e = getenv("MF_LEAF_KSUB")) ksub = atoi(e) == 1 ? 1 : 2;
+    CUtensorMap mA, mT, mB, mS;
+    const bool ok =
+        encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        encode_slot_view(&mT, a.T ? a.T : a.A, a.n_slots_a, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        encode_block_view(&mB, a.B, a.ldb, a.P, a.m, bn, BK * ksub, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+        encode_slot_view(&mS, a.S ? a.S : a.B, a.n_slots_b, a.m, bn, BK * ksub, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (!ok) return cudaErrorInvalidValue;
     LeafParams prm;
     prm.m = a.m;
     prm.tm0 = (int)(r0 / BM);
     prm.tiles_m = (int)tm_tiles;
     prm.tn0 = (int)(c0 / bn);
     prm.tiles_n = (int)((c1 - c0 + bn - 1) / bn);
-    prm.kblocks = (int)((a.m + BK - 1) / BK);
-    prm.bmode = bmode;
+    prm.kblocks = (int)((a.m + BK * ksub - 1) / (BK * ksub));
     prm.out = a.out;
     prm.ldo = a.ldo;
     prm.out_stride = a.out_block_stride;
@@ -522,10 +456,28 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.jobs = a.jobs;
     const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
-    if (bn == 64)
-      leaf_dmma_kernel<64><<<(unsigned)grid, THREADS, smem_bytes<64>(), s>>>(mA, mT, mB, mS, prm);
-    else
-      leaf_dmma_kernel<128><<<(unsigned)grid, THREADS, smem_bytes<128>(), s>>>(mA, mT, mB, mS, prm);
+    // the >48 KB dynamic shared memory opt-in is per device: once per
+    // (device, instantiation)
+    static std::atomic<uint64_t> attr_set[4];
+    const int inst = (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0);
+    const uint64_t dev_bit = 1ull << (dev & 63);
+    auto launch = [&](auto kern, int smem) -> cudaError_t {
+      if (!(attr_set[inst].load() & dev_bit)) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set[inst].fetch_or(dev_bit);
+      }
+      kern<<<(unsigned)grid, THREADS, smem, s>>>(mA, mT, mB, mS, prm);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    switch (inst) {
+      case 0: e = launch(leaf_dmma_kernel<128, 1>, smem_bytes<128, 1>()); break;
+      case 1: e = launch(leaf_dmma_kernel<128, 2>, smem_bytes<128, 2>()); break;
+      case 2: e = launch(leaf_dmma_kernel<64, 1>, smem_bytes<64, 1>()); break;
+      default: e = launch(leaf_dmma_kernel<64, 2>, smem_bytes<64, 2>()); break;
+    }
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
   SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, c0, c1, a.out, a.ldo,
