@@ -71,6 +71,7 @@ constexpr int GROUP_M = 8;
 
 struct LeafParams {
   int64_t m;
+  int group_m;  // tile-rows per rasterisation group
   int tm0, tn0;  // first tile row / column (region of the host-buffer pipeline)
   int tiles_m, tiles_n, kblocks;  // kblocks: stages of 16*KSUB k
   double* out;
@@ -159,9 +160,9 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int tiles_per_job = prm.tiles_m * prm.tiles_n;
   const int job_id = blockIdx.x / tiles_per_job;
   const int t = blockIdx.x - job_id * tiles_per_job;
-  const int group_tiles = GROUP_M * prm.tiles_n;
-  const int first_m = (t / group_tiles) * GROUP_M;
-  const int gsz = min(prm.tiles_m - first_m, GROUP_M);
+  const int group_tiles = prm.group_m * prm.tiles_n;
+  const int first_m = (t / group_tiles) * prm.group_m;
+  const int gsz = min(prm.tiles_m - first_m, prm.group_m);
   const int tm = prm.tm0 + first_m + (t % group_tiles) % gsz;
   const int tn = prm.tn0 + (t % group_tiles) / gsz;
   const LeafJob job = prm.jobs[job_id];
@@ -454,6 +455,8 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.out_stride = a.out_block_stride;
     prm.alpha = a.alpha;
     prm.jobs = a.jobs;
+    prm.group_m = GROUP_M;
+    if (const char* e = getenv("MF_LEAF_GROUPM")) prm.group_m = std::max(1, atoi(e));
     const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
