@@ -126,7 +126,7 @@ def config(a, world):
             "l2": ("inputs larger than L2 (8n^2 = %.1f GB per matrix); no flush" % (8 * a.n ** 2 / 1e9)
                    if 8 * a.n ** 2 > 126e6 else "inputs fit in L2 (%.1f MB per matrix); not flushed"
                    % (8 * a.n ** 2 / 1e6)),
-            "parallelism": f"product-sharded x{world}" if world > 1 else "single GPU"}
+            "parallelism": f"product-sharded x{world} (NCCL reduce of C)" if world > 1 else "single GPU"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -242,7 +242,7 @@ def run_reference(a):
     value = 2.0 * n ** 3 / dt / 1e12
     sample = (f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} per step "
               f"({(n / a.n) ** 3:.4g} of the n={a.n} work); value = 2n^3/t at n={n}")
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -250,11 +250,34 @@ def run_reference(a):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
+
+
+# ------------------------------------------------------------------ output
+_JSON_FD = None
+
+
+def _claim_stdout():
+    """Route fd 1 to stderr for the whole run (NCCL, torch or libraries may print
+    banners) and keep the real stdout for the one JSON line."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(obj):
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
 
 
 # ------------------------------------------------------------------ main arm
 def main():
+    _claim_stdout()
     a = parse()
     if a.impl == "reference":
         run_reference(a)
@@ -270,7 +293,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
+    # MF_BENCH_DIST=1 runs the distributed path even at world size 1 (process
+    # group, NCCL communicator through libmf, reduce of C, max-over-ranks
+    # timing) -- the multi-GPU plumbing, checkable on a single GPU
+    distributed = world > 1 or os.environ.get("MF_BENCH_DIST") == "1"
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
         obj = [mf.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -288,7 +315,7 @@ def main():
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -309,7 +336,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / a.steps
     phases = plan.profile_read(reset=True)
-    if world > 1:
+    if distributed:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -423,11 +450,11 @@ def main():
     plan.close()
     if comm is not None:
         mf.nccl_comm_destroy(comm)
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
 
 
 if __name__ == "__main__":

@@ -393,6 +393,26 @@ def test_split_sharding_partials_sum_to_product(N):
     assert scaled(host(total), ref, A, B) <= 2e-13
 
 
+def test_nccl_single_rank_plan_matches_local():
+    """The NCCL exchange step of the sharded path (mf_nccl_unique_id /
+    mf_nccl_comm_create / reduce of C in mf_dgemm) on a 1-rank communicator:
+    bitwise the local result; OUT_ALL (all-reduce) too; and IN_ROOT inputs are
+    broadcast into plan replicas."""
+    n = 512
+    A, B = mf_inputs.pair("uniform", n, 30)
+    with mf.Plan(triples.get(SW), 2, n) as p:
+        ref = host(p.dgemm(dev(A), dev(B)))
+    comm = mf.nccl_comm_create(mf.nccl_unique_id(), 0, 1)
+    try:
+        for out_mode, in_mode in ((mf.OUT_ROOT, mf.IN_REPLICATED), (mf.OUT_ALL, mf.IN_ROOT)):
+            with mf.Plan(triples.get(SW), 2, n, shard_rank=0, shard_count=1, nccl_comm=comm,
+                         output_mode=out_mode, input_mode=in_mode) as p:
+                C = host(p.dgemm(dev(A), dev(B)))
+            assert (C == ref).all()
+    finally:
+        mf.nccl_comm_destroy(comm)
+
+
 def run_plan(p, A, B):
     return host(p.dgemm(dev(A), dev(B)))
 
