@@ -400,8 +400,9 @@ def main():
             out["speedup_vs_cublas"] = t_cublas / ms
         del Cref
 
-    # ---- end to end through the C ABI with host buffers ----
-    if not a.no_e2e and world == 1:
+    # ---- end to end through the C ABI with host buffers (every rank: its
+    # replicated host inputs in, the NCCL reduce inside, C back; max over ranks) ----
+    if not a.no_e2e:
         Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         Bh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         Ch = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
@@ -409,13 +410,19 @@ def main():
         del A, B, C
         torch.cuda.empty_cache()
         plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)  # warm-up
+        barrier()
         t0 = time.perf_counter()
         for _ in range(a.steps):
             plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)
         dt = (time.perf_counter() - t0) / a.steps
+        if distributed:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
         out["e2e"] = {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "ms_per_step": dt * 1e3,
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
-                      "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step)"}
+                      "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step"
+                             + (", per rank, NCCL reduce inside)" if distributed else ")")}
         out["gpu_launches_e2e_per_step"] = 4 if a.levels > 0 else 1
 
     # ---- the same n with one more recursion level (deeper flattening), same run ----
