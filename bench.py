@@ -96,7 +96,9 @@ def parse():
     ap.add_argument("--max-workspace-gb", type=float, default=0.0,
                     help="cap the plan workspace (bounded schedule); 0 = unlimited")
     ap.add_argument("--no-variants", action="store_true",
-                    help="skip timing the deeper-flattening variant (same n, one more level)")
+                    help="skip timing the variants (same n: one more level; fused post-addition)")
+    ap.add_argument("--fuse", action="store_true",
+                    help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd)")
     a = ap.parse_args()
     if a.config:
         a.n, a.triple, a.levels = CONFIGS[a.config]
@@ -107,6 +109,8 @@ def parse():
 
 def workload_name(a):
     mode = "level by level" if getattr(a, "level_by_level", False) else "flattened"
+    if getattr(a, "fuse", False):
+        mode += ", post-additions fused into the leaf epilogue"
     return f"n={a.n} fp64, {a.levels}-level {a.triple} ({mode}, {_rank(a) ** a.levels} leaf products)"
 
 
@@ -307,7 +311,7 @@ def main():
     triple = resolve_triple(mf, a.triple)
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
                    nccl_comm=comm, profile=True, level_by_level=a.level_by_level,
-                   max_workspace=int(a.max_workspace_gb * 1e9))
+                   max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse)
     info = plan.info()
     stream = torch.cuda.current_stream()
     A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
@@ -364,8 +368,8 @@ def main():
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config(a, world), "clocks": clk,
-           "gpu_launches": (4 if a.levels > 0 else 1) * a.steps if not a.level_by_level
-                           else (2 + _rank(a) * 4 + 1) * a.steps,
+           "gpu_launches": ((3 if a.fuse else 4) if a.levels > 0 else 1) * a.steps
+                           if not a.level_by_level else (2 + _rank(a) * 4 + 1) * a.steps,
            "roofline": roofline}
 
     # ---- accuracy vs classical cuBLAS DGEMM, and the classical baselines ----
@@ -423,32 +427,40 @@ def main():
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
                       "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step"
                              + (", per rank, NCCL reduce inside)" if distributed else ")")}
-        out["gpu_launches_e2e_per_step"] = 4 if a.levels > 0 else 1
+        out["gpu_launches_e2e_per_step"] = (3 if a.fuse else 4) if a.levels > 0 else 1
 
-    # ---- the same n with one more recursion level (deeper flattening), same run ----
+    # ---- variants at the same n, same run: one more recursion level (deeper
+    # flattening), and the post-additions folded into the leaf epilogue ----
     if rank == 0 and world == 1 and not a.no_variants and a.triple == "strassen-winograd" \
-            and a.levels == 2 and not a.level_by_level and a.n % 8 == 0:
+            and a.levels == 2 and not a.level_by_level and not a.fuse and a.n % 8 == 0:
         torch.cuda.empty_cache()
         Av, Bv = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
         Cv = torch.empty((n, n), dtype=torch.float64, device=dev)
-        with mf.Plan(triple, 3, n, device=local) as p3:
-            for _ in range(a.warmup):
-                p3.dgemm(Av, Bv, Cv)
-            torch.cuda.synchronize()
-            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            v0.record(stream)
-            for _ in range(a.steps):
-                p3.dgemm(Av, Bv, Cv)
-            v1.record(stream)
-            torch.cuda.synchronize()
-            vms = v0.elapsed_time(v1) / a.steps
         Cr = torch.matmul(Av, Bv)
         den = n * float(Av.abs().max()) * float(Bv.abs().max())
-        err3 = float((Cv - Cr).abs().max()) / den
-        out["variants"] = [{"workload": f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)",
-                            "value": 2.0 * n ** 3 / (vms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": vms,
-                            "max_scaled_error": err3, "error_bound": 3e-13,
-                            "speedup_vs_cublas": (out.get("classical", {}).get("cublas_ms", 0) / vms) or None}]
+        out["variants"] = []
+        for label, levels, kw in (
+                (f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)", 3, {}),
+                (f"n={n} fp64, 2-level strassen-winograd, post-additions fused into the leaf "
+                 "epilogue (bulk f64 reductions into C, no P workspace)", 2, {"fuse_postadd": True})):
+            with mf.Plan(triple, levels, n, device=local, **kw) as pv:
+                for _ in range(a.warmup):
+                    pv.dgemm(Av, Bv, Cv)
+                torch.cuda.synchronize()
+                v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                v0.record(stream)
+                for _ in range(a.steps):
+                    pv.dgemm(Av, Bv, Cv)
+                v1.record(stream)
+                torch.cuda.synchronize()
+                vms = v0.elapsed_time(v1) / a.steps
+                ws = pv.info()["workspace_bytes"]
+            errv = float((Cv - Cr).abs().max()) / den
+            out["variants"].append({
+                "workload": label, "value": 2.0 * n ** 3 / (vms * 1e-3) / 1e12, "unit": UNIT,
+                "ms_per_step": vms, "max_scaled_error": errv, "error_bound": 1e-13 * levels,
+                "workspace_gb": ws / 1e9,
+                "speedup_vs_cublas": (out.get("classical", {}).get("cublas_ms", 0) / vms) or None})
         del Av, Bv, Cv, Cr
 
     if rank == 0 and world == 1 and not a.no_cpu:

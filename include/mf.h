@@ -85,6 +85,20 @@ typedef struct {
                            that fit (the paper's OOM at n=24012,
                            P:L489-492): per batch K4 on its slots, K5, K6 adding
                            into C.  Unsharded flattened plans only              */
+  int32_t fuse_postadd;   /* 1: fold the post-additions into the leaf epilogue
+                           (SURVEY §8a a4 / north_star (3): "optionally folded
+                           into the leaf GEMM epilogue so each product is
+                           accumulated straight into its C blocks").  C is
+                           zeroed, then every leaf tile adds alpha*W'[i][q]*P_q
+                           into each C block i it feeds with bulk f64 reductions
+                           (cp.reduce.async.bulk .add.f64).  No P workspace
+                           (saves R^L (n/p^L)^2 doubles); summation order across
+                           products is not fixed, so results are not bitwise
+                           reproducible (exact on integer-valued data within
+                           2^53).  Needs levels >= 1, flattened (not
+                           level_by_level), no batching, ldc even and C 16-byte
+                           aligned; else MF_ERR_UNSUPPORTED                     */
+  int32_t reserved0;      /* must be 0                                            */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.

@@ -223,6 +223,7 @@ void free_plan(Plan* pl) {
   for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_table,
                   (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
+                  (void*)pl->d_post_off, (void*)pl->d_post,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
@@ -269,6 +270,7 @@ mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B
   a.n_jobs = batch ? batch->n_jobs : (part ? pl.n_jobs_part : pl.n_jobs);
   if (batch) { a.n_slots_a = batch->n_a; a.n_slots_b = batch->n_b; }
   a.rows = rows;
+  if (pl.fuse && !batch && pl.levels > 0) { a.post_off = pl.d_post_off; a.post = pl.d_post; }
   MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
   return MF_OK;
 }
@@ -311,6 +313,11 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   }
   if (o.leaf != MF_LEAF_DMMA && o.leaf != MF_LEAF_SIMPLE)
     return fail(MF_ERR_INVALID_ARG, "unknown leaf kind %d", o.leaf);
+  if (o.reserved0 != 0) return fail(MF_ERR_INVALID_ARG, "mf_options.reserved0 must be 0");
+  if (o.fuse_postadd && levels < 1)
+    return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs levels >= 1");
+  if (o.fuse_postadd && o.level_by_level && levels >= 2)
+    return fail(MF_ERR_UNSUPPORTED, "fuse_postadd with level_by_level is not supported");
   const int shard_count = o.shard_count > 1 ? o.shard_count : 1;
   if (o.shard_rank < 0 || o.shard_rank >= shard_count)
     return fail(MF_ERR_INVALID_ARG, "shard_rank %d outside [0, %d)", o.shard_rank, shard_count);
@@ -366,7 +373,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   else pl->device = -1;
   pl->p = p; pl->R = R; pl->levels = levels; pl->n = n;
   pl->P = (int)P; pl->RL = RL; pl->m = n / P;
-  pl->opt = o; pl->leaf = o.leaf;
+  pl->opt = o; pl->leaf = o.leaf; pl->fuse = o.fuse_postadd != 0;
   pl->shard_rank = o.shard_rank; pl->shard_count = shard_count;
   pl->nccl_comm = o.nccl_comm;
 
@@ -478,7 +485,9 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   // ---- bounded workspace: batches of products whose T/S/P fit the cap ----
   const int64_t blk = (int64_t)sizeof(double) * pl->m * pl->m;
   if (levels > 0 && o.max_workspace > 0 &&
-      (int64_t)(pl->n_mat_a + pl->n_mat_b + RL) * blk > o.max_workspace) {
+      (int64_t)(pl->n_mat_a + pl->n_mat_b + (pl->fuse ? 0 : RL)) * blk > o.max_workspace) {
+    if (pl->fuse)
+      return fail(MF_ERR_UNSUPPORTED, "fuse_postadd: T/S workspace exceeds max_workspace (no batching)");
     if (shard_count > 1)
       return fail(MF_ERR_UNSUPPORTED, "max_workspace with product sharding is not supported");
     const int64_t g = o.max_workspace / (3 * blk);
@@ -535,7 +544,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     }
     if (tb && cudaMalloc(&pl->T, tb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace T (%zu bytes)", tb); }
     if (sb && cudaMalloc(&pl->S, sb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace S (%zu bytes)", sb); }
-    if (cudaMalloc(&pl->Pw, pb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace P (%zu bytes)", pb); }
+    if (pl->fuse) pb = 0;  // leaf tiles are added straight into C
+    if (pb && cudaMalloc(&pl->Pw, pb) != cudaSuccess) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "workspace P (%zu bytes)", pb); }
     pl->ws_bytes = tb + sb + pb;
     mf_status st;
     if ((st = upload_table(pl->mixA)) != MF_OK || (st = upload_table(pl->mixB)) != MF_OK ||
@@ -589,6 +599,34 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       return fail(MF_ERR_OUT_OF_MEMORY, "job table");
     }
     cudaMemcpy(pl->d_jobs, jobs.data(), sizeof(LeafJob) * jobs.size(), cudaMemcpyHostToDevice);
+  }
+  if (pl->fuse) {
+    // fused post-addition: product q feeds C block i with W'[i][q] (alias sign
+    // folded in); terms sorted by coefficient so each value is staged once
+    std::vector<int32_t> off(RL + 1, 0);
+    std::vector<PostTerm> terms;
+    std::vector<char> mine(RL, 0);
+    for (int32_t q : job_q) mine[q] = 1;
+    for (int64_t q = 0; q < RL; ++q) {
+      off[q] = (int32_t)terms.size();
+      if (!mine[q]) continue;
+      const size_t first = terms.size();
+      for (int i = 0; i < NB; ++i) {
+        const double w = pl->W[i * RL + q] * pl->prods[q].sign;
+        if (w != 0.0) terms.push_back(PostTerm{(int32_t)(((i / pl->P) << 16) | (i % pl->P)), 0, w});
+      }
+      std::stable_sort(terms.begin() + first, terms.end(),
+                       [](const PostTerm& x, const PostTerm& y) { return x.coef < y.coef; });
+    }
+    off[RL] = (int32_t)terms.size();
+    if (cudaMalloc(&pl->d_post_off, sizeof(int32_t) * off.size()) != cudaSuccess ||
+        (!terms.empty() && cudaMalloc(&pl->d_post, sizeof(PostTerm) * terms.size()) != cudaSuccess)) {
+      free_plan(pl.get());
+      return fail(MF_ERR_OUT_OF_MEMORY, "fused post-addition table");
+    }
+    cudaMemcpy(pl->d_post_off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice);
+    if (!terms.empty())
+      cudaMemcpy(pl->d_post, terms.data(), sizeof(PostTerm) * terms.size(), cudaMemcpyHostToDevice);
   }
   if (cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming) != cudaSuccess) {
     free_plan(pl.get());
@@ -717,6 +755,28 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
       mark(3);
       MF_CUDA(launch_postmix(*pl, b.mixC, alpha, pl->Pw, C, ldc, s, Rows(), bi > 0), "post-add (K6, batch)");
     }
+  } else if (pl->fuse) {
+    // fused post-addition: C = 0, then K4(A), K4(B) and the leaf, whose epilogue
+    // adds alpha * W'[i][q] * P_q into each C block i (no K6, no P workspace)
+    // (profile: the memset is timed with pre-add A)
+    MF_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, n * 8, n, s), "zero C");
+    MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
+    if (!pl->my_part.empty()) {
+      Rows pr;
+      pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
+      MF_CUDA(launch_premix(*pl, pl->mixA2, A, lda, pl->T, s, pr), "pre-add A (K4, split)");
+    }
+    mark(1);
+    MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
+    mark(2);
+    if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, C, ldc, 0, alpha, s)) != MF_OK) return st;
+    if (!pl->my_part.empty()) {
+      Rows pr;
+      pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
+      if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, C, ldc, 0, alpha, s, pr, true)) != MF_OK)
+        return st;
+    }
+    mark(3);
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
     MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
@@ -824,7 +884,7 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 // per element).
 static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
-      !pl.batches.empty())
+      !pl.batches.empty() || pl.fuse)
     return 1;
   const int64_t tiles = (pl.m + 127) / 128;
   return (int)std::min<int64_t>(8, tiles);

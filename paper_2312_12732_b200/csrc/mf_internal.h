@@ -43,6 +43,15 @@ struct LeafJob {
   int32_t out_idx;  // index of the output block in P (or 0 with direct C output)
 };
 
+// Fused post-addition (mf_options.fuse_postadd): product q's tiles are added
+// into C blocks post[post_off[q] .. post_off[q+1]) with coef*alpha; terms of one
+// product are sorted by coef so the epilogue restages its tile once per value.
+struct PostTerm {
+  int32_t blk;   // (block_row << 16) | block_col of the C block
+  int32_t pad;
+  double coef;   // W'[i][q] with the alias sign folded in
+};
+
 // Coefficient table of one mix kernel launch: nout outputs, each a
 // combination of up to nin inputs, coef[o * nin + k] (0 = absent).
 // Device form: MixRow[nrow] then MixTerm[nterm]; row o's terms are
@@ -105,7 +114,10 @@ struct Plan {
   // device memory
   double* T = nullptr;   // n_mat_a x m x m
   double* S = nullptr;   // n_mat_b x m x m
-  double* Pw = nullptr;  // RL x m x m (leaf outputs)
+  double* Pw = nullptr;  // RL x m x m (leaf outputs; not allocated when fused)
+  bool fuse = false;     // mf_options.fuse_postadd
+  int32_t* d_post_off = nullptr;  // RL + 1
+  PostTerm* d_post = nullptr;
   size_t ws_bytes = 0;
   LeafJob* d_jobs = nullptr;  // my_prods.size() jobs
   int n_jobs = 0;
@@ -157,6 +169,10 @@ struct LeafArgs {
   double alpha;
   const LeafJob* jobs; int n_jobs;
   Rows rows;      // output rows of each product computed (r0 multiple of 128)
+  // fused post-addition: post != nullptr => job q's tile is added into C
+  // (ldc) per post[post_off[out_idx] ..) instead of stored to out
+  const int32_t* post_off = nullptr;
+  const PostTerm* post = nullptr;
 };
 bool leaf_tma_supported(const LeafArgs& a);
 

@@ -78,6 +78,8 @@ struct LeafParams {
   int64_t ldo, out_stride;
   double alpha;
   const LeafJob* jobs;
+  const int32_t* post_off;  // fused post-addition (FUSE): out = C, ldo = ldc
+  const PostTerm* post;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -139,7 +141,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // BNT = CTA tile width (128, or 64 to cut wave quantisation on small batches):
 // warps form a 2 x 4 grid of 64 x (BNT/4) warp tiles, NJ = BNT/64 16-column
 // groups per warp.
-template <int BNT, int KSUB>
+template <int BNT, int KSUB, bool FUSE>
 __global__ void __launch_bounds__(THREADS, 1)
 leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
@@ -294,32 +296,87 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
   }
 
-  // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
-  double* out = prm.out + (int64_t)job.out_idx * prm.out_stride;
-  const double alpha = prm.alpha;
-  const bool vec_ok = ((prm.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 31) == 0);
+  if constexpr (FUSE) {
+    // ---- fused post-addition (north_star (3), "folded into the leaf GEMM
+    // epilogue"): stage coef*alpha*acc in the drained ring, then threads
+    // 0..127 each add one tile row into every C block product q feeds with a
+    // bulk f64 reduction (performed at L2; no P round trip through HBM) ----
+    constexpr int LDT = BNT + 2;  // +16 B per row: conflict-free v2 stores
+    static_assert(BM * LDT * 8 <= STAGES * STAGE_BYTES, "fused tile must fit the ring");
+    __syncthreads();  // every warp is past its last ring read; all TMA loads landed
+    double* tile = reinterpret_cast<double*>(smem);
+    const int q = job.out_idx;
+    const int t0 = prm.post_off[q], t1 = prm.post_off[q + 1];
+    const int64_t row0 = (int64_t)tm * BM, col0 = (int64_t)tn * BNT;
+    const int rows_valid = (int)min((int64_t)BM, prm.m - row0);
+    const int cols_valid = (int)min((int64_t)BNT, prm.m - col0);
+    double staged = 0.0;
+    for (int ti = t0; ti < t1; ++ti) {
+      const PostTerm pt = prm.post[ti];
+      const double c = pt.coef * prm.alpha;
+      if (ti == t0 || c != staged) {
+        if (ti > t0) {
+          if (threadIdx.x < BM) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncthreads();
+        }
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
-    if (row >= prm.m) continue;
+        for (int mi = 0; mi < 8; ++mi) {
+          const int r = wm * 64 + mi * 8 + lr;
 #pragma unroll
-    for (int nj = 0; nj < NJ; ++nj) {
-      const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
-      double v0 = acc[mi][nj][0][0], v1 = acc[mi][nj][1][0];
-      double v2 = acc[mi][nj][0][1], v3 = acc[mi][nj][1][1];
-      if (alpha != 1.0) {
-        v0 = __dmul_rn(alpha, v0); v1 = __dmul_rn(alpha, v1);
-        v2 = __dmul_rn(alpha, v2); v3 = __dmul_rn(alpha, v3);
+          for (int nj = 0; nj < NJ; ++nj) {
+            const int cc = wn * WN + nj * 16 + 4 * lk;
+            double* d = tile + r * LDT + cc;
+            const double v0 = c * acc[mi][nj][0][0], v1 = c * acc[mi][nj][1][0];
+            const double v2 = c * acc[mi][nj][0][1], v3 = c * acc[mi][nj][1][1];
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(smem_u32(d)), "d"(v0), "d"(v1) : "memory");
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};" :: "r"(smem_u32(d + 2)), "d"(v2), "d"(v3) : "memory");
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        staged = c;
       }
-      double* dst = out + row * prm.ldo + col;
-      if (vec_ok && col + 3 < prm.m) {
-        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
-                     :: "l"(dst), "d"(v0), "d"(v1), "d"(v2), "d"(v3) : "memory");
-      } else {
-        if (col + 0 < prm.m) dst[0] = v0;
-        if (col + 1 < prm.m) dst[1] = v1;
-        if (col + 2 < prm.m) dst[2] = v2;
-        if (col + 3 < prm.m) dst[3] = v3;
+      if ((int)threadIdx.x < rows_valid) {
+        const int64_t br = pt.blk >> 16, bc = pt.blk & 0xffff;
+        double* dst = prm.out + (br * prm.m + row0 + threadIdx.x) * prm.ldo + bc * prm.m + col0;
+        asm volatile(
+            "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+            :: "l"(dst), "r"(smem_u32(tile + threadIdx.x * LDT)), "r"(cols_valid * 8) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    // smem must outlive the bulk reads; the grid's completion covers the adds
+    // (waiting for their completion too measured the same: fused_postadd_r01.json)
+    if (threadIdx.x < BM) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    return;
+  } else {
+    // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
+    double* out = prm.out + (int64_t)job.out_idx * prm.out_stride;
+    const double alpha = prm.alpha;
+    const bool vec_ok = ((prm.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 31) == 0);
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
+      if (row >= prm.m) continue;
+#pragma unroll
+      for (int nj = 0; nj < NJ; ++nj) {
+        const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
+        double v0 = acc[mi][nj][0][0], v1 = acc[mi][nj][1][0];
+        double v2 = acc[mi][nj][0][1], v3 = acc[mi][nj][1][1];
+        if (alpha != 1.0) {
+          v0 = __dmul_rn(alpha, v0); v1 = __dmul_rn(alpha, v1);
+          v2 = __dmul_rn(alpha, v2); v3 = __dmul_rn(alpha, v3);
+        }
+        double* dst = out + row * prm.ldo + col;
+        if (vec_ok && col + 3 < prm.m) {
+          asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                       :: "l"(dst), "d"(v0), "d"(v1), "d"(v2), "d"(v3) : "memory");
+        } else {
+          if (col + 0 < prm.m) dst[0] = v0;
+          if (col + 1 < prm.m) dst[1] = v1;
+          if (col + 2 < prm.m) dst[2] = v2;
+          if (col + 3 < prm.m) dst[3] = v3;
+        }
       }
     }
   }
@@ -335,6 +392,8 @@ struct SimpleParams {
   int64_t ldo, out_stride;
   double alpha;
   const LeafJob* jobs;
+  const int32_t* post_off;  // fused post-addition: out = C, ldo = ldc
+  const PostTerm* post;
 };
 
 __global__ void leaf_simple_kernel(const SimpleParams prm) {
@@ -353,6 +412,14 @@ __global__ void leaf_simple_kernel(const SimpleParams prm) {
   else { Y = prm.B + (job.b_coord >> 16) * prm.m * prm.ldb + (job.b_coord & 0xffff) * prm.m; ldy = prm.ldb; }
   double acc = 0.0;
   for (int64_t k = 0; k < prm.m; ++k) acc = fma(X[r * ldx + k], Y[k * ldy + c], acc);
+  if (prm.post) {
+    for (int t = prm.post_off[job.out_idx]; t < prm.post_off[job.out_idx + 1]; ++t) {
+      const PostTerm pt = prm.post[t];
+      const int64_t br = pt.blk >> 16, bc = pt.blk & 0xffff;
+      atomicAdd(prm.out + (br * prm.m + r) * prm.ldo + bc * prm.m + c, pt.coef * prm.alpha * acc);
+    }
+    return;
+  }
   if (prm.alpha != 1.0) acc = __dmul_rn(prm.alpha, acc);
   prm.out[job.out_idx * prm.out_stride + r * prm.ldo + c] = acc;
 }
@@ -419,8 +486,10 @@ bool leaf_tma_supported(const LeafArgs& a) {
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m), c0 = a.rows.c0, c1 = a.rows.cend(a.m);
   if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cudaSuccess;
-  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && r0 % BM == 0 && c0 % BN == 0 &&
-      (c1 == a.m || c1 % BN == 0)) {
+  // fused post-addition: bulk reductions need 16-byte aligned C rows
+  const bool fuse_ok = !a.post || (!(a.ldo & 1) && al16(a.out));
+  if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && fuse_ok && r0 % BM == 0 &&
+      c0 % BN == 0 && (c1 == a.m || c1 % BN == 0)) {
     // Tile width: 64 when 128-wide tiles would leave a badly filled last wave
     // (e.g. 7 products of 2048^2: 12.1 waves of 148 SMs) -- model: wave fill
     // times a 2% per-tile penalty for the narrower tile (MF_LEAF_BN overrides).
@@ -436,6 +505,8 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (const char* e = getenv("MF_LEAF_BN")) bn = atoi(e) == 64 ? 64 : 128;
     int ksub = 2;  // k sub-blocks of 16 per pipeline stage
     if (const char* e = getenv("MF_LEAF_KSUB")) ksub = atoi(e) == 1 ? 1 : 2;
+    const bool fuse = a.post != nullptr;
+    if (fuse) ksub = 2;  // the fused tile is staged in the KSUB=2 ring
     CUtensorMap mA, mT, mB, mS;
     const bool ok =
         encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
@@ -455,14 +526,16 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.out_stride = a.out_block_stride;
     prm.alpha = a.alpha;
     prm.jobs = a.jobs;
+    prm.post_off = a.post_off;
+    prm.post = a.post;
     prm.group_m = GROUP_M;
     if (const char* e = getenv("MF_LEAF_GROUPM")) prm.group_m = std::max(1, atoi(e));
     const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)
-    static std::atomic<uint64_t> attr_set[4];
-    const int inst = (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0);
+    static std::atomic<uint64_t> attr_set[6];
+    const int inst = fuse ? (bn == 64 ? 5 : 4) : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0);
     const uint64_t dev_bit = 1ull << (dev & 63);
     auto launch = [&](auto kern, int smem) -> cudaError_t {
       if (!(attr_set[inst].load() & dev_bit)) {
@@ -475,16 +548,18 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     };
     cudaError_t e;
     switch (inst) {
-      case 0: e = launch(leaf_dmma_kernel<128, 1>, smem_bytes<128, 1>()); break;
-      case 1: e = launch(leaf_dmma_kernel<128, 2>, smem_bytes<128, 2>()); break;
-      case 2: e = launch(leaf_dmma_kernel<64, 1>, smem_bytes<64, 1>()); break;
-      default: e = launch(leaf_dmma_kernel<64, 2>, smem_bytes<64, 2>()); break;
+      case 0: e = launch(leaf_dmma_kernel<128, 1, false>, smem_bytes<128, 1>()); break;
+      case 1: e = launch(leaf_dmma_kernel<128, 2, false>, smem_bytes<128, 2>()); break;
+      case 2: e = launch(leaf_dmma_kernel<64, 1, false>, smem_bytes<64, 1>()); break;
+      case 3: e = launch(leaf_dmma_kernel<64, 2, false>, smem_bytes<64, 2>()); break;
+      case 4: e = launch(leaf_dmma_kernel<128, 2, true>, smem_bytes<128, 2>()); break;
+      default: e = launch(leaf_dmma_kernel<64, 2, true>, smem_bytes<64, 2>()); break;
     }
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
   SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, c0, c1, a.out, a.ldo,
-                   a.out_block_stride, a.alpha, a.jobs};
+                   a.out_block_stride, a.alpha, a.jobs, a.post_off, a.post};
   dim3 grid((unsigned)((c1 - c0 + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), (unsigned)a.n_jobs);
   leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
   return cudaGetLastError();

@@ -514,3 +514,86 @@ def test_bench_configs_full_size(name, levels, n):
         C = host(p.dgemm(Ad, Bd))
         A, B = host(Ad), host(Bd)
         _sampled_check(C, A, B, count=128, tol=1e-13 * levels)
+
+
+# ------------------------------------------------ fused post-addition (epilogue fold)
+
+FUSED_CASES = [(SW, 1, 256), (SW, 1, 400), (SW, 2, 512), (SW, 2, 800), (SW, 3, 1024),
+               ("paper-strassen", 2, 256), ("strassen-1969", 1, 256), ("laderman", 1, 390),
+               ("laderman", 2, 288), ("classical-p2", 1, 128)]
+
+
+@pytest.mark.parametrize("name,levels,n", FUSED_CASES)
+def test_fused_postadd_integer_exact_and_random(name, levels, n):
+    """North_star (3) / SURVEY §8a a4 "optionally folded into the leaf GEMM
+    epilogue": every product tile is added (bulk f64 reductions) into the C
+    blocks it feeds.  Integers: bit-exact (all partial sums exact, so order is
+    irrelevant); random: within the bound and close to the unfused path.
+    Covers -1 coefficients (restaged tile), ragged tails (n=400: m=200, n=800:
+    m=200, n=390: m=130), alpha != 1, and no P workspace."""
+    t = triples.get(name)
+    A, B = mf_inputs.pair("int1024", n, 40)
+    with mf.Plan(t, levels, n, fuse_postadd=True) as p:
+        C = torch.full((n, n), float("nan"), dtype=torch.float64, device="cuda")
+        assert (host(p.dgemm(dev(A), dev(B), C=C)) == exact(A, B)).all()
+        assert (host(p.dgemm(dev(A), dev(B), alpha=-2.0)) == -2.0 * exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 41)
+        Cf = host(p.dgemm(dev(A), dev(B), alpha=0.5))
+    with mf.Plan(t, levels, n) as p:
+        Cu = host(p.dgemm(dev(A), dev(B), alpha=0.5))
+    Cref = 0.5 * oracle.classical(A, B)
+    assert scaled(Cf, Cref, A, B) <= 1e-13 * levels
+    assert scaled(Cf, Cu, A, B) <= 1e-13 * levels
+
+
+def test_fused_postadd_workspace_views_and_fallbacks():
+    """Fused plans allocate no P workspace; strided C (ldc > n, even) keeps the
+    TMA/bulk path, odd ldc falls back to the simple leaf with f64 atomics; the
+    simple leaf kind and the host-buffer entry point work fused too."""
+    n, t = 512, triples.get(SW)
+    m = n // 4
+    with mf.Plan(t, 2, n) as p:
+        ws_unfused = p.info()["workspace_bytes"]
+    A, B = mf_inputs.pair("int1024", n, 42)
+    ref = exact(A, B)
+    with mf.Plan(t, 2, n, fuse_postadd=True) as p:
+        assert ws_unfused - p.info()["workspace_bytes"] == 49 * m * m * 8
+        for ldc in (n + 2, n + 1):
+            Cbig = torch.full((n, ldc), 7.0, dtype=torch.float64, device="cuda")
+            p.dgemm(dev(A), dev(B), C=Cbig[:, :n])
+            out = host(Cbig)
+            assert (out[:, :n] == ref).all() and (out[:, n:] == 7.0).all()
+        assert (p.dgemm_host(A, B) == ref).all()
+    with mf.Plan(t, 2, n, fuse_postadd=True, leaf="simple") as p:
+        assert (host(p.dgemm(dev(A), dev(B))) == ref).all()
+
+
+@pytest.mark.parametrize("N", [1, 3])
+def test_fused_postadd_sharded_partials(N):
+    """Fused epilogue on product shards, whole and split (row slabs): the
+    partial C of the N shards sum to the exact product."""
+    n = 2048
+    A, B = mf_inputs.pair("int1024", n, 43)
+    Ad, Bd = dev(A), dev(B)
+    total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N, fuse_postadd=True) as p:
+            total += p.dgemm(Ad, Bd)
+    assert (host(total) == exact(A, B)).all()
+
+
+def test_fused_postadd_bench_size_sampled():
+    """n = 16384, SW^2 fused (the bench's --fuse variant): Freivalds on integers
+    is exact; random inputs checked on sampled oracle entries."""
+    n = 16384
+    with mf.Plan(triples.get(SW), 2, n, fuse_postadd=True) as p:
+        Ad, Bd = mf_inputs.device_pair("int1024", n, 44)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+        del Ad, Bd
+        assert oracle.freivalds_int(A, B, C, trials=2) == 0
+        _sampled_check(C, A, B, count=128)
+        Ad, Bd = mf_inputs.device_pair("uniform", n, 45)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+    _sampled_check(C, A, B, count=128, tol=2e-13)
