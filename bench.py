@@ -97,6 +97,9 @@ def parse():
                     help="cap the plan workspace (bounded schedule); 0 = unlimited")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip timing the variants (same n: one more level; fused post-addition)")
+    ap.add_argument("--recurse-levels", type=int, default=0,
+                    help="with --level-by-level: top levels run one at a time (0 = all but the "
+                         "last); the rest run as one flattened child plan")
     ap.add_argument("--fuse", action="store_true",
                     help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd)")
     a = ap.parse_args()
@@ -109,9 +112,29 @@ def parse():
 
 def workload_name(a):
     mode = "level by level" if getattr(a, "level_by_level", False) else "flattened"
+    if getattr(a, "level_by_level", False) and getattr(a, "recurse_levels", 0):
+        r = a.recurse_levels
+        mode = (f"{r} top level(s) one at a time, each product a flattened "
+                f"{a.levels - r}-level child")
     if getattr(a, "fuse", False):
         mode += ", post-additions fused into the leaf epilogue"
     return f"n={a.n} fp64, {a.levels}-level {a.triple} ({mode}, {_rank(a) ** a.levels} leaf products)"
+
+
+def launches_per_step(a):
+    """Our kernels per mf_dgemm: K4, K4, K5, K6 per flattened level (K6 folded
+    into K5 with --fuse); level by level: the top level's K4, K4, K6 around R
+    child calls."""
+    if a.levels == 0:
+        return 1
+    flat = 3 if a.fuse else 4
+    if not a.level_by_level or a.levels < 2:
+        return flat
+    r = a.recurse_levels if 0 < a.recurse_levels < a.levels else a.levels - 1
+    count = flat
+    for _ in range(r):
+        count = 3 + _rank(a) * count
+    return count
 
 
 def _rank(a):
@@ -311,7 +334,8 @@ def main():
     triple = resolve_triple(mf, a.triple)
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
                    nccl_comm=comm, profile=True, level_by_level=a.level_by_level,
-                   max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse)
+                   max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse,
+                   recurse_levels=a.recurse_levels)
     info = plan.info()
     stream = torch.cuda.current_stream()
     A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
@@ -368,8 +392,7 @@ def main():
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config(a, world), "clocks": clk,
-           "gpu_launches": ((3 if a.fuse else 4) if a.levels > 0 else 1) * a.steps
-                           if not a.level_by_level else (2 + _rank(a) * 4 + 1) * a.steps,
+           "gpu_launches": launches_per_step(a) * a.steps,
            "roofline": roofline}
 
     # ---- accuracy vs classical cuBLAS DGEMM, and the classical baselines ----
@@ -427,7 +450,7 @@ def main():
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
                       "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step"
                              + (", per rank, NCCL reduce inside)" if distributed else ")")}
-        out["gpu_launches_e2e_per_step"] = (3 if a.fuse else 4) if a.levels > 0 else 1
+        out["gpu_launches_e2e_per_step"] = launches_per_step(a)
 
     # ---- variants at the same n, same run: one more recursion level (deeper
     # flattening), and the post-additions folded into the leaf epilogue ----

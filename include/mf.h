@@ -96,9 +96,15 @@ typedef struct {
                            products is not fixed, so results are not bitwise
                            reproducible (exact on integer-valued data within
                            2^53).  Needs levels >= 1, flattened (not
-                           level_by_level), no batching, ldc even and C 16-byte
-                           aligned; else MF_ERR_UNSUPPORTED                     */
-  int32_t reserved0;      /* must be 0                                            */
+                           level_by_level) and no batching, else
+                           MF_ERR_UNSUPPORTED.  Odd ldc or C not 16-byte aligned
+                           run the simple leaf with f64 atomics instead       */
+  int32_t recurse_levels; /* with level_by_level = 1: how many top levels run one
+                           at a time (0 = levels - 1, the paper's full
+                           recursion); the remaining levels run as ONE
+                           flattened child plan, e.g. levels = 4,
+                           recurse_levels = 1: one level of R products, each a
+                           flattened 3-level product (R^3 leaves in one launch) */
 } mf_options;
 
 /* mf_plan -- validate and prepare <U,V,W> applied `levels` times at size n.

@@ -313,7 +313,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   }
   if (o.leaf != MF_LEAF_DMMA && o.leaf != MF_LEAF_SIMPLE)
     return fail(MF_ERR_INVALID_ARG, "unknown leaf kind %d", o.leaf);
-  if (o.reserved0 != 0) return fail(MF_ERR_INVALID_ARG, "mf_options.reserved0 must be 0");
+  if (o.recurse_levels < 0)
+    return fail(MF_ERR_INVALID_ARG, "recurse_levels must be >= 0 (got %d)", o.recurse_levels);
   if (o.fuse_postadd && levels < 1)
     return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs levels >= 1");
   if (o.fuse_postadd && o.level_by_level && levels >= 2)
@@ -338,8 +339,13 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   if (o.level_by_level && levels >= 2) {
     // the paper's recursion: this plan = one level; each of its R products is
     // computed by a child plan of levels - 1 levels at n / p
+    // top `r` levels one at a time; below them one flattened child plan
+    const int r = (o.recurse_levels <= 0 || o.recurse_levels >= levels) ? levels - 1 : o.recurse_levels;
     mf_options top = o, sub = o;
     top.level_by_level = 0;
+    top.recurse_levels = 0;
+    sub.level_by_level = r > 1 ? 1 : 0;
+    sub.recurse_levels = r > 1 ? r - 1 : 0;
     sub.shard_rank = 0; sub.shard_count = 1; sub.nccl_comm = nullptr; sub.profile = 0;
     sub.input_mode = MF_IN_REPLICATED;
     mf_plan_t parent = nullptr, child = nullptr;

@@ -168,14 +168,15 @@ def test_product_kron_matches_oracle_kron():
 
 def test_fused_postadd_option_validation():
     """mf_options.fuse_postadd (include/mf.h): needs levels >= 1 and the flattened
-    path; reserved0 must be 0; both are checked before any device work."""
+    path; recurse_levels must be >= 0; all checked before any device work."""
     t = triples.STRASSEN_WINOGRAD
     st, msg = _plan_status(2, 7, t.U, t.V, t.W, 0, 64, fuse_postadd=1, host_only=1)
     assert st == mf.MF_ERR_UNSUPPORTED and "levels" in msg
     st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, fuse_postadd=1, level_by_level=1, host_only=1)
     assert st == mf.MF_ERR_UNSUPPORTED and "level_by_level" in msg
-    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, reserved0=1, host_only=1)
-    assert st == mf.MF_ERR_INVALID_ARG and "reserved0" in msg
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, level_by_level=1, recurse_levels=-1,
+                           host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "recurse_levels" in msg
     p = mf.Plan(t, 2, 64, fuse_postadd=True, host_only=True)
     assert p.info()["n_products"] == 49
     p.close()

@@ -319,6 +319,25 @@ def test_level_by_level_recursion(name, levels, n):
     assert scaled(C, 1.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
 
 
+@pytest.mark.parametrize("name,levels,n,r", [(SW, 3, 512, 1), (SW, 4, 1024, 1), (SW, 4, 2048, 2),
+                                             ("laderman", 3, 27 * 16, 1)])
+def test_recurse_levels_hybrid(name, levels, n, r):
+    """level_by_level with recurse_levels = r: the top r levels one at a time,
+    each product a flattened (levels - r)-level child plan.  Same bilinear map:
+    exact on integers; random within the bound and close to the oracle's
+    recursion."""
+    t = triples.get(name)
+    A, B = mf_inputs.pair("int1024", n, 46)
+    with mf.Plan(t, levels, n, level_by_level=True, recurse_levels=r) as p:
+        assert p.info()["n_products"] == t.R and p.info()["leaf_n"] == n // t.p
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 47)
+        C = host(p.dgemm(dev(A), dev(B), alpha=-0.5))
+    Co = oracle.fmm(A, B, oracle.catalog(name), levels, alpha=-0.5)
+    assert scaled(C, Co, A, B) <= 1e-13 * levels
+    assert scaled(C, -0.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
+
+
 def test_config1_n64_sw1_all_distributions():
     """BASELINE config 1: n=64, one-level Strassen-Winograd."""
     for kind in ("int8", "int1024"):
