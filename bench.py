@@ -32,16 +32,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "effective fp64 TFLOPS (2n^3/t) at n=16384 vs classic DGEMM; max scaled error"
 UNIT = "TFLOPS"
-CPU_SAMPLE_N = 4096  # oracle sample: same triple and levels at n/4 (1/64 of the work)
+CPU_SAMPLE_N = 4096  # reference-arm step: same triple and levels at n/4 (1/64 of the work)
+CPU_BASELINE_N = 8192  # cpu_baseline leg: n/2 (1/8 of the work, ~15-20 s on 16 cores)
 
 
-def cpu_sample_n(a):
-    """n of the bounded oracle sample: n/4 capped at 4096, divisible by p^levels."""
+def cpu_sample_n(a, div=4, cap=CPU_SAMPLE_N):
+    """n of a bounded oracle sample: n/div capped at `cap`, divisible by p^levels."""
     p = 1
     for part in a.triple.split("(x)"):
         p *= {"laderman": 3, "classical-p3": 3}.get(part, 2)
     p = p ** a.levels
-    ns = min(max(a.n // 4, p), CPU_SAMPLE_N)
+    ns = min(max(a.n // div, p), cap)
     return max(p, ns - ns % p)
 
 
@@ -63,7 +64,13 @@ CONFIGS = {
     "x-ldsw-13824": (13824, "laderman(x)strassen-winograd", 1),
     # bounded workspace (NEXT-3): n where the all-products workspace does not fit in HBM
     "x-sw2-49152-bounded": (49152, "strassen-winograd", 2),
+    # four levels: one level of SW run level by level, each of its 7 products a
+    # flattened SW^3 child plan (343 leaves in one launch); mf_options.recurse_levels
+    "x-sw4-16384-hybrid": (16384, "strassen-winograd", 4),
+    "x-sw4-32768-hybrid": (32768, "strassen-winograd", 4),
 }
+# presets run level by level with this many recursive top levels
+PRESET_RECURSE = {"x-sw4-16384-hybrid": 1, "x-sw4-32768-hybrid": 1}
 # presets that need a workspace cap (GB): 49152^2 * 8 B = 19.3 GB per matrix;
 # all 129 T/S/P blocks (1.2 GB each) would need 156 GB on top of A, B, C, C_ref
 PRESET_WORKSPACE_GB = {"x-sw2-49152-bounded": 85.0}
@@ -107,6 +114,8 @@ def parse():
         a.n, a.triple, a.levels = CONFIGS[a.config]
         if a.config in PRESET_WORKSPACE_GB and not a.max_workspace_gb:
             a.max_workspace_gb = PRESET_WORKSPACE_GB[a.config]
+        if a.config in PRESET_RECURSE:
+            a.level_by_level, a.recurse_levels = True, PRESET_RECURSE[a.config]
     return a
 
 
@@ -231,11 +240,12 @@ def oracle_triple(a):
 
 def cpu_baseline(a):
     """The oracle (or_fmm: plain C interpreter of Eq. "strassen", OpenMP over
-    rows) on the host cores: same triple and levels at n = CPU_SAMPLE_N."""
+    rows) on the host cores: same triple and levels at n/2 (<= CPU_BASELINE_N),
+    about 10-30 s of CPU work."""
     import numpy as np
     import mf_inputs
     import oracle
-    n = cpu_sample_n(a)
+    n = cpu_sample_n(a, div=2, cap=CPU_BASELINE_N)
     A, B = mf_inputs.pair("uniform", n, 0)
     t = oracle_triple(a)
     t0 = time.perf_counter()
@@ -464,8 +474,13 @@ def main():
         out["variants"] = []
         for label, levels, kw in (
                 (f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)", 3, {}),
+                (f"n={n} fp64, 4-level strassen-winograd (one level by level, each of its 7 "
+                 "products a flattened <8,8,8;343> child: 2401 leaves)", 4,
+                 {"level_by_level": True, "recurse_levels": 1}),
                 (f"n={n} fp64, 2-level strassen-winograd, post-additions fused into the leaf "
                  "epilogue (bulk f64 reductions into C, no P workspace)", 2, {"fuse_postadd": True})):
+            if n % (2 ** levels):
+                continue
             with mf.Plan(triple, levels, n, device=local, **kw) as pv:
                 for _ in range(a.warmup):
                     pv.dgemm(Av, Bv, Cv)

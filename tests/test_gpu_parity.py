@@ -338,6 +338,24 @@ def test_recurse_levels_hybrid(name, levels, n, r):
     assert scaled(C, -0.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
 
 
+def test_sw4_hybrid_bench_size_sampled():
+    """The bench's 4-level variant at full size (n = 16384: one SW level by
+    level over 7 flattened SW^3 children, 2401 leaves of 1024^2): exact
+    Freivalds on integers, sampled oracle entries on random inputs."""
+    n = 16384
+    with mf.Plan(triples.get(SW), 4, n, level_by_level=True, recurse_levels=1) as p:
+        Ad, Bd = mf_inputs.device_pair("int1024", n, 48)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+        del Ad, Bd
+        assert oracle.freivalds_int(A, B, C, trials=2) == 0
+        _sampled_check(C, A, B, count=128)
+        Ad, Bd = mf_inputs.device_pair("uniform", n, 49)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+    _sampled_check(C, A, B, count=128, tol=4e-13)
+
+
 def test_config1_n64_sw1_all_distributions():
     """BASELINE config 1: n=64, one-level Strassen-Winograd."""
     for kind in ("int8", "int1024"):
