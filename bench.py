@@ -107,6 +107,8 @@ def parse():
     ap.add_argument("--recurse-levels", type=int, default=0,
                     help="with --level-by-level: top levels run one at a time (0 = all but the "
                          "last); the rest run as one flattened child plan")
+    ap.add_argument("--leaf", choices=["dmma", "cublas", "simple"], default="dmma",
+                    help="leaf GEMM: our TMA+DMMA kernel (default) or the cuBLAS ablation")
     ap.add_argument("--fuse", action="store_true",
                     help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd)")
     a = ap.parse_args()
@@ -127,6 +129,8 @@ def workload_name(a):
                 f"{a.levels - r}-level child")
     if getattr(a, "fuse", False):
         mode += ", post-additions fused into the leaf epilogue"
+    if getattr(a, "leaf", "dmma") != "dmma":
+        mode += f", {a.leaf} leaf (ablation)"
     return f"n={a.n} fp64, {a.levels}-level {a.triple} ({mode}, {_rank(a) ** a.levels} leaf products)"
 
 
@@ -345,7 +349,7 @@ def main():
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
                    nccl_comm=comm, profile=True, level_by_level=a.level_by_level,
                    max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse,
-                   recurse_levels=a.recurse_levels)
+                   recurse_levels=a.recurse_levels, leaf=a.leaf)
     info = plan.info()
     stream = torch.cuda.current_stream()
     A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
@@ -392,7 +396,9 @@ def main():
         leaf_flops = R ** a.levels * 2.0 * (n // p ** a.levels) ** 3
     peak, peak_src = fp64_peak()
     achieved = leaf_flops / (leaf_ms * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "leaf_dmma_kernel (K5)", "achieved": achieved,
+    kernel = {"dmma": "leaf_dmma_kernel (K5)", "cublas": "cublasDgemmBatched leaf (ablation)",
+              "simple": "leaf_simple_kernel (ablation)"}[a.leaf]
+    roofline = {"bound": "tensor", "kernel": kernel, "achieved": achieved,
                 "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": leaf_traffic(),
                 "peak_source": peak_src, "flops_per_launch": leaf_flops, "ms_per_launch": leaf_ms,
                 "phase_ms_per_step": {k: phases[k] / max(1, phases["calls"]) for k in plan.PHASES},

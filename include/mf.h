@@ -49,15 +49,20 @@ typedef enum {
 
 typedef struct mf_plan_st* mf_plan_t;
 
-enum { MF_LEAF_DMMA = 0, MF_LEAF_SIMPLE = 1 };
+enum { MF_LEAF_DMMA = 0, MF_LEAF_SIMPLE = 1, MF_LEAF_CUBLAS = 2 };
 enum { MF_IN_ROOT = 0, MF_IN_REPLICATED = 1 };
-enum { MF_OUT_ROOT = 0, MF_OUT_ALL = 1 };
+enum { MF_OUT_ROOT = 0, MF_OUT_ALL = 1, MF_OUT_ROWSLAB = 2 };
 
 typedef struct {
   int32_t struct_size;  /* sizeof(mf_options); 0-initialised struct = defaults    */
   int32_t device;       /* CUDA device ordinal; -1 = current device (default)     */
   int32_t leaf;         /* MF_LEAF_DMMA (default): TMA + mma.sync f64 leaf GEMM;
-                           MF_LEAF_SIMPLE: plain fp64 FMA leaf (test ablation)    */
+                           MF_LEAF_SIMPLE: plain fp64 FMA leaf (test ablation);
+                           MF_LEAF_CUBLAS: the R^L leaf products as
+                           cublasDgemmBatched calls, one per operand-stride
+                           group (ablation: same K4/K6, library leaf;
+                           libcublas.so.12 is dlopen'ed, MF_ERR_CUDA if absent;
+                           not with fuse_postadd)                              */
   int32_t shard_rank;   /* product sharding: this rank's index (default 0)        */
   int32_t shard_count;  /* number of shards; 0/1 = unsharded.  With nccl_comm ==
                            NULL a sharded plan computes only its shard's PARTIAL C
@@ -65,8 +70,12 @@ typedef struct {
   void* nccl_comm;      /* ncclComm_t from mf_nccl_comm_create, or NULL           */
   int32_t input_mode;   /* MF_IN_REPLICATED (inputs valid on every rank) or
                            MF_IN_ROOT (rank 0's A, B are broadcast first)         */
-  int32_t output_mode;  /* MF_OUT_ROOT (C summed onto rank 0) or MF_OUT_ALL
-                           (C summed onto every rank)                             */
+  int32_t output_mode;  /* MF_OUT_ROOT (C summed onto rank 0), MF_OUT_ALL (C
+                           summed onto every rank) or MF_OUT_ROWSLAB (rank r
+                           receives rows [r*n/N, (r+1)*n/N) of the sum; its C
+                           argument is that n/N x n slab, ldc == n; needs
+                           n % N == 0; the full partial C lives in a
+                           plan-owned buffer).  Only with nccl_comm           */
   int32_t profile;      /* 1: mf_dgemm records CUDA events around each phase on
                            the call's stream (read with mf_profile_read)          */
   int32_t host_only;    /* 1: plan the host logic only (Brent check, flattening,

@@ -33,9 +33,9 @@ MF_ERR_OUT_OF_MEMORY, MF_ERR_CUDA, MF_ERR_NCCL, MF_ERR_UNSUPPORTED = 4, 5, 6, 7
 STATUS_NAMES = {0: "MF_OK", 1: "MF_ERR_INVALID_ARG", 2: "MF_ERR_INDIVISIBLE",
                 3: "MF_ERR_BAD_TRIPLE", 4: "MF_ERR_OUT_OF_MEMORY", 5: "MF_ERR_CUDA",
                 6: "MF_ERR_NCCL", 7: "MF_ERR_UNSUPPORTED"}
-LEAF_DMMA, LEAF_SIMPLE = 0, 1
+LEAF_DMMA, LEAF_SIMPLE, LEAF_CUBLAS = 0, 1, 2
 IN_ROOT, IN_REPLICATED = 0, 1
-OUT_ROOT, OUT_ALL = 0, 1
+OUT_ROOT, OUT_ALL, OUT_ROWSLAB = 0, 1, 2
 
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
@@ -93,13 +93,15 @@ def version() -> str:
     return _lib.mf_version().decode()
 
 
-def _mat(X, n, name):
-    """(pointer, leading dimension) of a row-major n x n float64 CUDA tensor view."""
+def _mat(X, n, name, rows=None):
+    """(pointer, leading dimension) of a row-major n x n (or rows x n) float64
+    CUDA tensor view."""
     import torch
+    rows = n if rows is None else rows
     if not isinstance(X, torch.Tensor) or not X.is_cuda or X.dtype != torch.float64:
         raise TypeError(f"{name} must be a CUDA float64 tensor")
-    if X.dim() != 2 or tuple(X.shape) != (n, n) or X.stride(1) != 1:
-        raise ValueError(f"{name} must be an n x n row-major view (n={n}), got "
+    if X.dim() != 2 or tuple(X.shape) != (rows, n) or X.stride(1) != 1:
+        raise ValueError(f"{name} must be a {rows} x {n} row-major view, got "
                          f"shape {tuple(X.shape)} strides {X.stride()}")
     return X.data_ptr(), X.stride(0)
 
@@ -123,7 +125,7 @@ class Plan:
         opt = mf_options()
         opt.struct_size = ctypes.sizeof(mf_options)
         opt.device = -1 if device is None else int(device)
-        opt.leaf = {"dmma": LEAF_DMMA, "simple": LEAF_SIMPLE}[leaf]
+        opt.leaf = {"dmma": LEAF_DMMA, "simple": LEAF_SIMPLE, "cublas": LEAF_CUBLAS}[leaf]
         opt.shard_rank, opt.shard_count = int(shard_rank), int(shard_count)
         opt.nccl_comm = nccl_comm.value if isinstance(nccl_comm, ctypes.c_void_p) else nccl_comm
         opt.input_mode, opt.output_mode = int(input_mode), int(output_mode)
@@ -188,25 +190,33 @@ class Plan:
         n = self.n
         pa, lda = _mat(A, n, "A") if A is not None else (None, n)
         pb, ldb = _mat(B, n, "B") if B is not None else (None, n)
+        rows = self.c_rows()
         if C is None:
             dev = A.device if A is not None else torch.device("cuda")
-            C = torch.empty((n, n), dtype=torch.float64, device=dev)
-        pc, ldc = _mat(C, n, "C")
+            C = torch.empty((rows, n), dtype=torch.float64, device=dev)
+        pc, ldc = _mat(C, n, "C", rows)
         _check(_lib.mf_dgemm(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
                              _stream_ptr(stream)))
         return C
 
+    def c_rows(self) -> int:
+        """Rows of this rank's C: n, or n / shard_count with MF_OUT_ROWSLAB."""
+        o = self._opt
+        if o.output_mode == OUT_ROWSLAB and o.nccl_comm and o.shard_count > 1:
+            return self.n // o.shard_count
+        return self.n
+
     def dgemm_host(self, A: np.ndarray, B: np.ndarray, C: np.ndarray | None = None,
                    alpha: float = 1.0, stream=None) -> np.ndarray:
         """The same product on HOST float64 row-major arrays (copies inside the call)."""
-        def host(X, name):
-            if X.dtype != np.float64 or X.ndim != 2 or X.shape != (self.n, self.n) or \
+        def host(X, name, rows=self.n):
+            if X.dtype != np.float64 or X.ndim != 2 or X.shape != (rows, self.n) or \
                     X.strides[1] != 8:
-                raise ValueError(f"{name} must be a row-major {self.n}x{self.n} float64 array")
+                raise ValueError(f"{name} must be a row-major {rows}x{self.n} float64 array")
             return X.ctypes.data, X.strides[0] // 8
         if C is None:
-            C = np.empty((self.n, self.n))
-        pa, lda = host(A, "A"); pb, ldb = host(B, "B"); pc, ldc = host(C, "C")
+            C = np.empty((self.c_rows(), self.n))
+        pa, lda = host(A, "A"); pb, ldb = host(B, "B"); pc, ldc = host(C, "C", self.c_rows())
         _check(_lib.mf_dgemm_host(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
                                   _stream_ptr(stream)))
         return C

@@ -70,6 +70,8 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -90,12 +92,42 @@ Nccl* nccl() {
     n.Reduce = (decltype(n.Reduce))dlsym(h, "ncclReduce");
     n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
     n.Broadcast = (decltype(n.Broadcast))dlsym(h, "ncclBroadcast");
+    n.ReduceScatter = (decltype(n.ReduceScatter))dlsym(h, "ncclReduceScatter");
     n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
     n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
     n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
   });
-  return n.h && n.GetUniqueId && n.CommInitRank && n.Reduce && n.AllReduce && n.Broadcast ? &n
-                                                                                        : nullptr;
+  return n.h && n.GetUniqueId && n.CommInitRank && n.Reduce && n.AllReduce && n.Broadcast &&
+                 n.ReduceScatter
+             ? &n
+             : nullptr;
+}
+
+// ------------------------------------------------- cuBLAS (dlopen; MF_LEAF_CUBLAS)
+// The leaf ablation only: the library DGEMM on the same K4/K6 pipeline.
+struct Cublas {
+  void* h = nullptr;
+  int (*Create)(void**) = nullptr;
+  int (*Destroy)(void*) = nullptr;
+  int (*SetStream)(void*, cudaStream_t) = nullptr;
+  int (*DgemmBatched)(void*, int, int, int, int, int, const double*, const double* const*, int,
+                      const double* const*, int, const double*, double* const*, int, int) = nullptr;
+};
+
+Cublas* cublas() {
+  static Cublas c;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    c.h = h;
+    c.Create = (decltype(c.Create))dlsym(h, "cublasCreate_v2");
+    c.Destroy = (decltype(c.Destroy))dlsym(h, "cublasDestroy_v2");
+    c.SetStream = (decltype(c.SetStream))dlsym(h, "cublasSetStream_v2");
+    c.DgemmBatched = (decltype(c.DgemmBatched))dlsym(h, "cublasDgemmBatched");
+  });
+  return c.h && c.Create && c.Destroy && c.SetStream && c.DgemmBatched ? &c : nullptr;
 }
 
 mf_status nccl_fail(Nccl* n, ncclResult_t r, const char* what) {
@@ -223,10 +255,11 @@ void free_plan(Plan* pl) {
   for (void* p : {(void*)pl->T, (void*)pl->S, (void*)pl->Pw, (void*)pl->d_jobs, (void*)pl->mixA.d_table,
                   (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
-                  (void*)pl->d_post_off, (void*)pl->d_post,
+                  (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
+  if (pl->cublas) cublas()->Destroy(pl->cublas);
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
@@ -251,16 +284,87 @@ cudaEvent_t* prof_slot(Plan* pl) {
   return pl->prof_events[pl->prof_used++].data();
 }
 
-bool overlaps(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t n) {
-  auto lo1 = reinterpret_cast<uintptr_t>(X), hi1 = lo1 + 8 * ((n - 1) * ldx + n);
-  auto lo2 = reinterpret_cast<uintptr_t>(Y), hi2 = lo2 + 8 * ((n - 1) * ldy + n);
+// do the address ranges of X (rx rows) and Y (ry rows), n columns each, intersect?
+bool overlaps(const double* X, int64_t ldx, int64_t rx, const double* Y, int64_t ldy, int64_t ry,
+              int64_t n) {
+  auto lo1 = reinterpret_cast<uintptr_t>(X), hi1 = lo1 + 8 * ((rx - 1) * ldx + n);
+  auto lo2 = reinterpret_cast<uintptr_t>(Y), hi2 = lo2 + 8 * ((ry - 1) * ldy + n);
   return lo1 < hi2 && lo2 < hi1;
+}
+
+// MF_LEAF_CUBLAS: row-major P = X*Y is column-major P^T = Y^T X^T, so each
+// product is cublasDgemm(N, N, cols, rows, m, Y, ldy, X, ldx, P, ldo); jobs are
+// grouped by (ldx, ldy) (aliased operands have ld n, workspace slots ld m).
+mf_status run_leaf_cublas(Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
+                          const double* T, const double* S, double* out, int64_t ldo,
+                          int64_t stride, double alpha, cudaStream_t s, Rows rows, int j0, int nj) {
+  Cublas* cb = cublas();
+  if (!cb) return fail(MF_ERR_CUDA, "MF_LEAF_CUBLAS: libcublas.so.12 could not be loaded");
+  if (!pl.cublas && cb->Create(&pl.cublas) != 0) return fail(MF_ERR_CUDA, "cublasCreate failed");
+  if (cb->SetStream(pl.cublas, s) != 0) return fail(MF_ERR_CUDA, "cublasSetStream failed");
+  const int64_t m = pl.m, mm = m * m;
+  const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
+  if (nj == 0 || r1 <= r0 || c1 <= c0) return MF_OK;
+  if (m > INT32_MAX || lda > INT32_MAX || ldb > INT32_MAX || ldo > INT32_MAX)
+    return fail(MF_ERR_UNSUPPORTED, "MF_LEAF_CUBLAS: dimensions exceed int32");
+  struct Group { int64_t ldx, ldy; std::vector<const double*> x, y, p; };
+  std::vector<Group> groups;
+  for (int j = j0; j < j0 + nj; ++j) {
+    const LeafJob& jb = pl.h_jobs[j];
+    const bool aw = jb.flags & 1, bw = jb.flags & 2;
+    const double* X = aw ? T + (int64_t)jb.a_coord * mm
+                         : A + (int64_t)(jb.a_coord >> 16) * m * lda + (int64_t)(jb.a_coord & 0xffff) * m;
+    const double* Y = bw ? S + (int64_t)jb.b_coord * mm
+                         : B + (int64_t)(jb.b_coord >> 16) * m * ldb + (int64_t)(jb.b_coord & 0xffff) * m;
+    const int64_t ldx = aw ? m : lda, ldy = bw ? m : ldb;
+    Group* g = nullptr;
+    for (auto& e : groups)
+      if (e.ldx == ldx && e.ldy == ldy) g = &e;
+    if (!g) { groups.push_back(Group{ldx, ldy, {}, {}, {}}); g = &groups.back(); }
+    g->x.push_back(X + r0 * ldx);
+    g->y.push_back(Y + c0);
+    g->p.push_back(out + (int64_t)jb.out_idx * stride + r0 * ldo + c0);
+  }
+  const size_t need = 3 * (size_t)nj;
+  if (pl.d_ptrs_cap < need) {
+    if (pl.d_ptrs) cudaFree(pl.d_ptrs);
+    pl.d_ptrs = nullptr; pl.d_ptrs_cap = 0;
+    MF_CUDA(cudaMalloc(&pl.d_ptrs, need * sizeof(double*)), "cudaMalloc(pointer arrays)");
+    pl.d_ptrs_cap = need;
+  }
+  std::vector<const double*> host;
+  host.reserve(need);
+  for (auto& g : groups) {
+    host.insert(host.end(), g.y.begin(), g.y.end());
+    host.insert(host.end(), g.x.begin(), g.x.end());
+    host.insert(host.end(), g.p.begin(), g.p.end());
+  }
+  // pageable source: the copy is staged before the call returns
+  MF_CUDA(cudaMemcpyAsync(pl.d_ptrs, host.data(), host.size() * sizeof(double*),
+                          cudaMemcpyHostToDevice, s), "H2D pointer arrays");
+  const double beta = 0.0;
+  size_t off = 0;
+  for (auto& g : groups) {
+    const int cnt = (int)g.x.size();
+    const double* const* dy = pl.d_ptrs + off;
+    const double* const* dx = dy + cnt;
+    double* const* dp = const_cast<double* const*>(dx + cnt);
+    if (cb->DgemmBatched(pl.cublas, 0, 0, (int)(c1 - c0), (int)(r1 - r0), (int)m, &alpha, dy,
+                         (int)g.ldy, dx, (int)g.ldx, &beta, dp, (int)ldo, cnt) != 0)
+      return fail(MF_ERR_CUDA, "cublasDgemmBatched failed");
+    off += 3 * (size_t)cnt;
+  }
+  return MF_OK;
 }
 
 mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B, int64_t ldb,
                    const double* T, const double* S, double* out, int64_t ldo, int64_t stride,
                    double alpha, cudaStream_t s, Rows rows = Rows(), bool part = false,
                    const Plan::Batch* batch = nullptr) {
+  if (pl.leaf == MF_LEAF_CUBLAS)
+    return run_leaf_cublas(const_cast<Plan&>(pl), A, lda, B, ldb, T, S, out, ldo, stride, alpha, s,
+                           rows, batch ? batch->job0 : (part ? pl.n_jobs : 0),
+                           batch ? batch->n_jobs : (part ? pl.n_jobs_part : pl.n_jobs));
   LeafArgs a;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
   a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
@@ -311,8 +415,17 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
                   (int)sizeof(mf_options));
     o = *opt;
   }
-  if (o.leaf != MF_LEAF_DMMA && o.leaf != MF_LEAF_SIMPLE)
+  if (o.leaf != MF_LEAF_DMMA && o.leaf != MF_LEAF_SIMPLE && o.leaf != MF_LEAF_CUBLAS)
     return fail(MF_ERR_INVALID_ARG, "unknown leaf kind %d", o.leaf);
+  if (o.output_mode != MF_OUT_ROOT && o.output_mode != MF_OUT_ALL && o.output_mode != MF_OUT_ROWSLAB)
+    return fail(MF_ERR_INVALID_ARG, "unknown output_mode %d", o.output_mode);
+  if (o.input_mode != MF_IN_ROOT && o.input_mode != MF_IN_REPLICATED)
+    return fail(MF_ERR_INVALID_ARG, "unknown input_mode %d", o.input_mode);
+  if (o.output_mode == MF_OUT_ROWSLAB && o.shard_count > 1 && n % o.shard_count != 0)
+    return fail(MF_ERR_INVALID_ARG, "MF_OUT_ROWSLAB needs n %% shard_count == 0 (n = %lld, N = %d)",
+                (long long)n, o.shard_count);
+  if (o.fuse_postadd && o.leaf == MF_LEAF_CUBLAS)
+    return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs the DMMA or simple leaf");
   if (o.recurse_levels < 0)
     return fail(MF_ERR_INVALID_ARG, "recurse_levels must be >= 0 (got %d)", o.recurse_levels);
   if (o.fuse_postadd && levels < 1)
@@ -445,7 +558,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     if (pl->prods[q].shard < 0) pl->my_part.push_back((int32_t)q);
   }
 
-  // unsharded plans of a compiled-in triple use the specialised K4/K6
+  // plans of a compiled-in triple use the specialised K4/K6 (sharded plans:
+  // masked to their own products; slots keep the full numbering)
   if (levels > 0 && RL <= 576 && !getenv("MF_MIX_GENERIC")) {
     pl->fixed_id = fixed_match(*pl);
     if (pl->fixed_id == 0) pl->fixed_id = kron_match(*pl);
@@ -606,6 +720,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     }
     cudaMemcpy(pl->d_jobs, jobs.data(), sizeof(LeafJob) * jobs.size(), cudaMemcpyHostToDevice);
   }
+  pl->h_jobs = jobs;
   if (pl->fuse) {
     // fused post-addition: product q feeds C block i with W'[i][q] (alias sign
     // folded in); terms sorted by coefficient so each value is staged once
@@ -704,9 +819,13 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
     if ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK)
       return st;
   }
+  // MF_OUT_ROWSLAB: C is this rank's n/N x n row slab of the reduced product
+  const bool rowslab = pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB;
+  const int64_t c_rows = rowslab ? n / pl->shard_count : n;
   if ((st = check_mat("C", C, ldc, n)) != MF_OK) return st;
-  if ((A && overlaps(A, lda, C, ldc, n)) || (B && overlaps(B, ldb, C, ldc, n)))
+  if ((A && overlaps(A, lda, n, C, ldc, c_rows, n)) || (B && overlaps(B, ldb, n, C, ldc, c_rows, n)))
     return fail(MF_ERR_INVALID_ARG, "C overlaps A or B");
+  if (rowslab && ldc != n) return fail(MF_ERR_UNSUPPORTED, "MF_OUT_ROWSLAB needs ldc == n");
   DeviceGuard guard(pl->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
@@ -731,6 +850,13 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
     if ((r = nc->Broadcast(pl->hB, pl->hB, (size_t)n * n, ncclDouble, 0, comm, s)) != ncclSuccess)
       return nccl_fail(nc, r, "ncclBroadcast(B)");
     A = pl->hA; lda = n; B = pl->hB; ldb = n;
+  }
+
+  double* const C_out = C;
+  if (rowslab) {  // compute the full partial C in a plan buffer, reduce-scatter it below
+    if (!pl->Cfull && cudaMalloc(&pl->Cfull, sizeof(double) * n * n) != cudaSuccess)
+      return fail(MF_ERR_OUT_OF_MEMORY, "partial C buffer (MF_OUT_ROWSLAB)");
+    C = pl->Cfull;
   }
 
   cudaEvent_t* ev = prof_slot(pl);
@@ -844,9 +970,11 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
     // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
     ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
     if (ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");
-    ncclResult_t r = pl->opt.output_mode == MF_OUT_ALL
-                         ? nc->AllReduce(C, C, (size_t)n * n, ncclDouble, ncclSum, comm, s)
-                         : nc->Reduce(C, C, (size_t)n * n, ncclDouble, ncclSum, 0, comm, s);
+    ncclResult_t r =
+        rowslab ? nc->ReduceScatter(C, C_out, (size_t)c_rows * n, ncclDouble, ncclSum, comm, s)
+        : pl->opt.output_mode == MF_OUT_ALL
+            ? nc->AllReduce(C, C, (size_t)n * n, ncclDouble, ncclSum, comm, s)
+            : nc->Reduce(C, C, (size_t)n * n, ncclDouble, ncclSum, 0, comm, s);
     if (r != ncclSuccess) return nccl_fail(nc, r, "ncclReduce(C)");
   }
   mark(5);
@@ -927,7 +1055,9 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
     pl->opt = saved;
     if (st != MF_OK) return st;
-    MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, n, cudaMemcpyDeviceToHost, s), "D2H C");
+    const int64_t c_rows =
+        pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB ? n / pl->shard_count : n;
+    MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, s), "D2H C");
     MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return MF_OK;
   }

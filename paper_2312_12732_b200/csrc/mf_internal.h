@@ -120,6 +120,11 @@ struct Plan {
   PostTerm* d_post = nullptr;
   size_t ws_bytes = 0;
   LeafJob* d_jobs = nullptr;  // my_prods.size() jobs
+  std::vector<LeafJob> h_jobs;  // host copy (MF_LEAF_CUBLAS builds pointer arrays from it)
+  void* cublas = nullptr;       // cublasHandle_t (MF_LEAF_CUBLAS), created on first use
+  const double** d_ptrs = nullptr;  // device pointer arrays for cublasDgemmBatched
+  size_t d_ptrs_cap = 0;
+  double* Cfull = nullptr;      // MF_OUT_ROWSLAB: the full partial C before reduce-scatter
   int n_jobs = 0;
   // host-buffer path (mf_dgemm_host): device copies of A, B, C
   double *hA = nullptr, *hB = nullptr, *hC = nullptr;

@@ -180,3 +180,22 @@ def test_fused_postadd_option_validation():
     p = mf.Plan(t, 2, 64, fuse_postadd=True, host_only=True)
     assert p.info()["n_products"] == 49
     p.close()
+
+
+def test_output_mode_and_leaf_validation():
+    """MF_OUT_ROWSLAB needs n % shard_count == 0; unknown modes/leaf kinds and
+    fuse_postadd with the cuBLAS leaf are rejected on the host."""
+    t = triples.STRASSEN_WINOGRAD
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, output_mode=mf.OUT_ROWSLAB, shard_count=3,
+                           host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "ROWSLAB" in msg
+    st, _ = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, output_mode=mf.OUT_ROWSLAB, shard_count=4,
+                         host_only=1)
+    assert st == mf.MF_OK
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, output_mode=7, host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "output_mode" in msg
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, leaf=9, host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "leaf" in msg
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, leaf=mf.LEAF_CUBLAS, fuse_postadd=1,
+                           host_only=1)
+    assert st == mf.MF_ERR_UNSUPPORTED

@@ -634,3 +634,54 @@ def test_fused_postadd_bench_size_sampled():
         C = host(p.dgemm(Ad, Bd))
         A, B = host(Ad), host(Bd)
     _sampled_check(C, A, B, count=128, tol=2e-13)
+
+
+# ------------------------------------------------ cuBLAS leaf ablation, row-slab output
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 1, 256), (SW, 2, 512), ("laderman", 1, 390),
+                                           (None, 0, 300), (SW, 3, 1024)])
+def test_cublas_leaf_ablation(name, levels, n):
+    """MF_LEAF_CUBLAS: the same K4/K6 around cublasDgemmBatched leaf products
+    (grouped by operand strides).  Integers exact; random within the bound."""
+    t = triples.get(name) if name else None
+    A, B = mf_inputs.pair("int1024", n, 50)
+    with mf.Plan(t, levels, n, leaf="cublas") as p:
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 51)
+        C = host(p.dgemm(dev(A), dev(B), alpha=0.25))
+        assert (p.dgemm_host(A, B, alpha=0.25) == C).all()
+    assert scaled(C, 0.25 * oracle.classical(A, B), A, B) <= 1e-13 * max(1, levels)
+
+
+def test_cublas_leaf_split_sharding_and_batches():
+    """The cuBLAS leaf on split-product row slabs (shards) and bounded-workspace
+    batches (batch-local slots): partials sum / results equal the exact product."""
+    n = 1024
+    A, B = mf_inputs.pair("int1024", n, 52)
+    total = np.zeros((n, n))
+    for r in range(3):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=3, leaf="cublas") as p:
+            total += run_plan(p, A, B)
+    assert (total == exact(A, B)).all()
+    m = n // 4
+    with mf.Plan(triples.get(SW), 2, n, leaf="cublas", max_workspace=3 * 5 * m * m * 8) as p:
+        assert (run_plan(p, A, B) == exact(A, B)).all()
+
+
+def test_nccl_rowslab_output_single_rank():
+    """MF_OUT_ROWSLAB: C reduce-scattered by block rows (ncclReduceScatter); on a
+    1-rank communicator the slab is the whole product, bitwise the local result,
+    through both entry points."""
+    n = 512
+    A, B = mf_inputs.pair("uniform", n, 53)
+    with mf.Plan(triples.get(SW), 2, n) as p:
+        ref = host(p.dgemm(dev(A), dev(B)))
+    comm = mf.nccl_comm_create(mf.nccl_unique_id(), 0, 1)
+    try:
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=0, shard_count=1, nccl_comm=comm,
+                     output_mode=mf.OUT_ROWSLAB, input_mode=mf.IN_REPLICATED) as p:
+            assert p.c_rows() == n
+            assert (host(p.dgemm(dev(A), dev(B))) == ref).all()
+            assert (p.dgemm_host(A, B) == ref).all()
+    finally:
+        mf.nccl_comm_destroy(comm)
