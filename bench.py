@@ -242,6 +242,16 @@ def oracle_triple(a):
     return t
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(a):
     """The oracle (or_fmm: plain C interpreter of Eq. "strassen", OpenMP over
     rows) on the host cores: same triple and levels at n/2 (<= CPU_BASELINE_N),
@@ -252,11 +262,20 @@ def cpu_baseline(a):
     n = cpu_sample_n(a, div=2, cap=CPU_BASELINE_N)
     A, B = mf_inputs.pair("uniform", n, 0)
     t = oracle_triple(a)
+    # load the library and start its OpenMP pool (~1 s in a process that
+    # imported torch) outside the timed region
+    oracle.classical(A[:64, :64], B[:64, :64])
     t0 = time.perf_counter()
     oracle.fmm(A, B, t, a.levels)
     dt = time.perf_counter() - t0
+    nc = min(n, 4096)  # O3, the plain classical loop, on the same cores
+    t0 = time.perf_counter()
+    oracle.classical(A[:nc, :nc], B[:nc, :nc])
+    dtc = time.perf_counter() - t0
     return {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "cores": oracle.num_threads(),
-            "kind": "oracle",
+            "kind": "oracle", "cpu_model": _cpu_model(),
+            "classical_o3": {"n": nc, "seconds": dtc, "value": 2.0 * nc ** 3 / dtc / 1e12,
+                             "unit": UNIT},
             "sample": f"or_fmm({a.triple}, levels={a.levels}) full call at n={n} "
                       f"({(n / a.n) ** 3:.4g} of the n={a.n} work), {dt:.2f} s; value = 2n^3/t at n={n}",
             "seconds": dt}
@@ -484,7 +503,9 @@ def main():
                  "products a flattened <8,8,8;343> child: 2401 leaves)", 4,
                  {"level_by_level": True, "recurse_levels": 1}),
                 (f"n={n} fp64, 2-level strassen-winograd, post-additions fused into the leaf "
-                 "epilogue (bulk f64 reductions into C, no P workspace)", 2, {"fuse_postadd": True})):
+                 "epilogue (bulk f64 reductions into C, no P workspace)", 2, {"fuse_postadd": True}),
+                (f"n={n} fp64, 2-level strassen-winograd with cuBLAS-batched leaves (ablation: "
+                 "same K4/K6, cublasDgemmBatched leaf)", 2, {"leaf": "cublas"})):
             if n % (2 ** levels):
                 continue
             with mf.Plan(triple, levels, n, device=local, **kw) as pv:
