@@ -256,6 +256,7 @@ void free_plan(Plan* pl) {
                   (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
+                  (void*)pl->split_ws, (void*)pl->split_cnt,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
@@ -375,6 +376,24 @@ mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B
   if (batch) { a.n_slots_a = batch->n_a; a.n_slots_b = batch->n_b; }
   a.rows = rows;
   if (pl.fuse && !batch && pl.levels > 0) { a.post_off = pl.d_post_off; a.post = pl.d_post; }
+  if (pl.leaf == MF_LEAF_DMMA) {
+    // split-K tail workspace: grown to what this launch's tiling needs
+    const LeafTiles cfg = leaf_tiles(a);
+    Plan& mp = const_cast<Plan&>(pl);
+    if (cfg.split > 1 && (mp.split_ws_elems < cfg.ws_elems || mp.split_cnt_len < cfg.n_tail)) {
+      MF_CUDA(cudaStreamSynchronize(s), "sync before workspace growth");
+      if (mp.split_ws) cudaFree(mp.split_ws);
+      if (mp.split_cnt) cudaFree(mp.split_cnt);
+      mp.split_ws = nullptr; mp.split_cnt = nullptr; mp.split_ws_elems = mp.split_cnt_len = 0;
+      MF_CUDA(cudaMalloc(&mp.split_ws, sizeof(double) * cfg.ws_elems), "cudaMalloc(split-K workspace)");
+      MF_CUDA(cudaMalloc(&mp.split_cnt, sizeof(int) * cfg.n_tail), "cudaMalloc(split-K counters)");
+      MF_CUDA(cudaMemset(mp.split_cnt, 0, sizeof(int) * cfg.n_tail), "zero split-K counters");
+      mp.split_ws_elems = cfg.ws_elems;
+      mp.split_cnt_len = cfg.n_tail;
+    }
+    a.split_ws = mp.split_ws; a.split_ws_elems = mp.split_ws_elems;
+    a.split_cnt = mp.split_cnt; a.split_cnt_len = mp.split_cnt_len;
+  }
   MF_CUDA(launch_leaf(a, pl.leaf, s), "leaf kernel launch");
   return MF_OK;
 }
@@ -1015,7 +1034,8 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 //   d2h  : each finished C region
 // Compute starts after 1/NS + 1/NC of an input crossed PCIe; everything else
 // overlaps.  Results are bitwise those of mf_dgemm (same kernels, same order
-// per element).
+// per element) unless mf_dgemm's leaf cut a few-wave launch's tail into
+// split-K pieces (region launches never split); then they agree to rounding.
 static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
       !pl.batches.empty() || pl.fuse)

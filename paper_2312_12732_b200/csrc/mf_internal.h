@@ -125,6 +125,10 @@ struct Plan {
   const double** d_ptrs = nullptr;  // device pointer arrays for cublasDgemmBatched
   size_t d_ptrs_cap = 0;
   double* Cfull = nullptr;      // MF_OUT_ROWSLAB: the full partial C before reduce-scatter
+  double* split_ws = nullptr;   // leaf split-K tail: partial tiles (grown on demand)
+  int64_t split_ws_elems = 0;
+  int* split_cnt = nullptr;     // ... and arrival counters (zeroed at allocation)
+  int64_t split_cnt_len = 0;
   int n_jobs = 0;
   // host-buffer path (mf_dgemm_host): device copies of A, B, C
   double *hA = nullptr, *hB = nullptr, *hC = nullptr;
@@ -178,8 +182,23 @@ struct LeafArgs {
   // (ldc) per post[post_off[out_idx] ..) instead of stored to out
   const int32_t* post_off = nullptr;
   const PostTerm* post = nullptr;
+  // split-K tail workspace (plan-owned; sized from leaf_tiles): partial tiles
+  // and per-tail-tile arrival counters (zero between launches)
+  double* split_ws = nullptr;
+  int64_t split_ws_elems = 0;
+  int* split_cnt = nullptr;
+  int64_t split_cnt_len = 0;
 };
 bool leaf_tma_supported(const LeafArgs& a);
+// tile width and split-K tail chosen for a DMMA leaf launch (mf_leaf.cu)
+struct LeafTiles {
+  int bn = 128;
+  int split = 1;         // k-range pieces per tail tile (1 = none)
+  int64_t n_whole = 0;   // tiles computed whole (first blocks of the grid)
+  int64_t n_tail = 0;    // tiles computed as `split` pieces each
+  int64_t ws_elems = 0;  // doubles of partial-tile workspace needed
+};
+LeafTiles leaf_tiles(const LeafArgs& a);
 
 // mf_fixed.cu: compile-time specialised K4/K6 for the catalog triples
 int fixed_match(const Plan& pl);

@@ -16,23 +16,26 @@
 //    TMA zero-fills past the block edge (ragged leaves never read a
 //    neighbouring block); a materialised operand is a slot of the T/S
 //    workspace (3-D map {col, row, slot}).
-//  * CTA tile 128x128x16.  Each MMA warp owns 64x32 of C: 64 fp64
-//    accumulators per thread.  Fragments are fetched with 128-bit LDS, which
-//    shared memory serves per quarter-warp (8 lanes): conflict-free needs the
-//    8 lanes of a quarter to hit 8 distinct 16-byte bank groups.
-//      Both tiles are TMA-written with SWIZZLE_128B in rows of 16 doubles
-//      (A: [128 m][16 k]; B: 8 boxes of [16 k][16 n]); physical 16-byte chunk
-//      = logical chunk ^ (row & 7).
-//      A: lane (r=L/4, kk=L%4) loads the k-pair chunk c(kk,g) of row r;
-//      B: lane (kk, nn=L/4) loads B[2c(kk,g)+s][2nn], B[..][2nn+1] (n-pair).
-//      The k-permutation k = 2c(kk,g) + s with c(.,0) = {0,3,5,6},
-//      c(.,1) = {1,2,4,7} makes both conflict-free: A needs one chunk of
-//      every pair {2j,2j+1} (rows 2q, 2q+1 share a quarter), B needs c mod 4
-//      distinct (its four k rows must land on four different XOR masks).
-//      Each k-step s feeds one DMMA; the n-permutation n = 2c + j of B makes
-//      each thread own 4 CONSECUTIVE output columns (one 256-bit store).
-//  * Grid = products x tiles, 1 CTA/SM (256 threads, ~164 KB smem); tiles of
-//    a product are rasterised in groups of 8 tile-rows for L2 reuse.
+//  * CTA tile 128 x BNT (BNT = 128, or 64 for badly filled last waves), k 32
+//    per ring stage (KSUB = 2 sub-blocks of 16; 3 stages in 192 KB).  Each
+//    MMA warp owns 64 x BNT/4 of C: 64 fp64 accumulators per thread at
+//    BNT = 128.  Fragments are fetched with 128-bit LDS, which shared memory
+//    serves per quarter-warp (8 lanes).
+//      A is TMA-written with SWIZZLE_128B in rows of 16 doubles ([128 m][16 k]
+//      per sub-block; physical 16-byte chunk = logical chunk ^ (row & 7)); lane
+//      (r=L/4, kk=L%4) loads the k-pair chunk c(kk,g) of row r.  The
+//      k-permutation k = 2c(kk,g) + s with c(.,0) = {0,3,5,6}, c(.,1) =
+//      {1,2,4,7} takes one chunk of every pair {2j,2j+1}: conflict-free.
+//      B is one unswizzled [32 k][BNT n] box per stage; lane (kk, nn=L/4)
+//      loads B[2c(kk,g)+s][2nn..2nn+1] (4-way conflicted; the swizzled
+//      alternatives measured slower, see below).  The n-permutation n = 2c + j
+//      gives each thread 4 CONSECUTIVE output columns (one 256-bit store).
+//  * Grid = products x tiles, 1 CTA/SM (256 threads, 192 KB ring); tiles of a
+//    product are rasterised in groups of 8 tile-rows for L2 reuse.
+//  * Split-K tail: when the tiles fill the SMs in few waves, the last
+//    (partial) waves' tiles are cut into S k-ranges; each piece stores its
+//    partial accumulators and the last piece to finish sums the S partials in
+//    split order (deterministic) and runs the normal epilogue.
 #include <cuda.h>
 
 #include <atomic>
@@ -80,6 +83,11 @@ struct LeafParams {
   const LeafJob* jobs;
   const int32_t* post_off;  // fused post-addition (FUSE): out = C, ldo = ldc
   const PostTerm* post;
+  // split-K tail: blocks >= n_whole are pieces (tile n_whole + (b - n_whole) / split,
+  // k-range (b - n_whole) % split); partials in part_ws, arrivals in part_cnt
+  int n_whole, split;
+  double* part_ws;
+  int* part_cnt;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -158,10 +166,20 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t full0 = s_base + STAGES * STAGE_BYTES;
   const uint32_t empty0 = full0 + STAGES * 8;
 
+  // ---- block -> tile (whole, or one k-range piece of a tail tile) ----
+  const bool piece = !FUSE && prm.split > 1 && (int)blockIdx.x >= prm.n_whole;
+  int tile = blockIdx.x, split_idx = 0, kb0 = 0, nk = prm.kblocks;
+  if (piece) {
+    const int pc = blockIdx.x - prm.n_whole;
+    tile = prm.n_whole + pc / prm.split;
+    split_idx = pc % prm.split;
+    kb0 = split_idx * prm.kblocks / prm.split;
+    nk = (split_idx + 1) * prm.kblocks / prm.split - kb0;
+  }
   // ---- tile -> (product job, tm, tn), grouped rasterisation ----
   const int tiles_per_job = prm.tiles_m * prm.tiles_n;
-  const int job_id = blockIdx.x / tiles_per_job;
-  const int t = blockIdx.x - job_id * tiles_per_job;
+  const int job_id = tile / tiles_per_job;
+  const int t = tile - job_id * tiles_per_job;
   const int group_tiles = prm.group_m * prm.tiles_n;
   const int first_m = (t / group_tiles) * prm.group_m;
   const int gsz = min(prm.tiles_m - first_m, prm.group_m);
@@ -187,8 +205,8 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const CUtensorMap* mapB = b_ws ? &tmS : &tmB;
   const int a_br = job.a_coord >> 16, a_bc = job.a_coord & 0xffff;
   const int b_br = job.b_coord >> 16, b_bc = job.b_coord & 0xffff;
-  auto issue = [&](int kb) {
-    const int s = kb % STAGES;
+  auto issue = [&](int i) {  // i: stage of this block's k-range; k block kb0 + i
+    const int s = i % STAGES, kb = kb0 + i;
     const uint32_t fb = full0 + 8 * s;
     mbar_expect_tx(fb, STAGE_BYTES);
     const uint32_t dA = s_base + s * STAGE_BYTES, dB = dA + A_BYTES;
@@ -203,7 +221,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" :: "l"(reinterpret_cast<uint64_t>(mapB)) : "memory");
-    for (int kb = 0; kb < STAGES - 1 && kb < prm.kblocks; ++kb) issue(kb);
+    for (int i = 0; i < STAGES - 1 && i < nk; ++i) issue(i);
   }
 
   // ================= MMA warps =================
@@ -262,14 +280,14 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             dmma(acc[mi][nj][j][0], acc[mi][nj][j][1], fa[mi][s2], fb[nj][s2][j]);
   };
 
-  if (prm.kblocks > 0) {
+  if (nk > 0) {
     mbar_wait(full0, 0);
     load_frags(s_base, s_base + A_BYTES, 0, fa0, fb0);
   }
-  for (int kb = 0; kb < prm.kblocks; ++kb) {
+  for (int kb = 0; kb < nk; ++kb) {  // kb: stage index within this block's k-range
     if (warp == 0) {
       const int kn = kb + STAGES - 1;  // refill the slot consumed at kb - 1
-      if (kn < prm.kblocks) {
+      if (kn < nk) {
         if (kb > 0) mbar_wait(empty0 + 8 * (kn % STAGES), ((kb - 1) / STAGES) & 1);
         if (lane == 0) issue(kn);
       }
@@ -285,7 +303,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       } else {                               // last group: release, prefetch next stage
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * s);
-        if (kb + 1 < prm.kblocks) {
+        if (kb + 1 < nk) {
           const int s1 = (kb + 1) % STAGES;
           mbar_wait(full0 + 8 * s1, ((kb + 1) / STAGES) & 1);
           const uint32_t nA = s_base + s1 * STAGE_BYTES;
@@ -350,6 +368,42 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (threadIdx.x < BM) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     return;
   } else {
+    if (piece) {
+      // ---- split-K piece: publish the partial, the last arrival reduces ----
+      constexpr int NACC = 8 * NJ * 4;
+      const int tail = tile - prm.n_whole;
+      double* ws = prm.part_ws + ((size_t)tail * prm.split + split_idx) * (NACC * THREADS);
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = (mi * NJ + nj) * 4 + u;
+            __stcg(ws + e * THREADS + threadIdx.x, acc[mi][nj][u >> 1][u & 1]);
+          }
+      __threadfence();
+      __syncthreads();
+      __shared__ int s_last;
+      if (threadIdx.x == 0) s_last = atomicAdd(prm.part_cnt + tail, 1) == prm.split - 1;
+      __syncthreads();
+      if (!s_last) return;
+      __threadfence();
+      const double* base = prm.part_ws + (size_t)tail * prm.split * (NACC * THREADS);
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = (mi * NJ + nj) * 4 + u;
+            double v = __ldcg(base + e * THREADS + threadIdx.x);
+            for (int sp = 1; sp < prm.split; ++sp)
+              v += __ldcg(base + ((size_t)sp * NACC + e) * THREADS + threadIdx.x);
+            acc[mi][nj][u >> 1][u & 1] = v;
+          }
+      if (threadIdx.x == 0) prm.part_cnt[tail] = 0;  // ready for the next launch
+    }
     // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
     double* out = prm.out + (int64_t)job.out_idx * prm.out_stride;
     const double alpha = prm.alpha;
@@ -483,6 +537,58 @@ bool leaf_tma_supported(const LeafArgs& a) {
   return true;
 }
 
+// Tile shape and split-K tail of one DMMA leaf launch.  Cost model in units of
+// one 128x128 tile's time, waves of `sms` CTAs:
+//  * BN = 128: ceil(tiles / sms);  BN = 64: ceil(tiles64 / sms) * 0.5 / 0.98
+//    (2% per-tile penalty for the narrower tile);
+//  * split-K (BN = 128): the first w full waves whole, the remaining tiles cut
+//    into S k-ranges: w + ceil(tail * S / sms) * (1 / S + eps), eps = the
+//    per-piece overhead (prologue + partial store/reload, ~4 us against a
+//    0.13 us-per-k tile).
+// E.g. 7 products of 2048^2 (config 2): 1792 tiles = 12.1 waves -> 12 whole
+// waves + 16 tiles x 9 pieces (12.13) instead of 25 half-width waves (12.76).
+// MF_LEAF_BN / MF_LEAF_SPLIT override.
+LeafTiles leaf_tiles(const LeafArgs& a) {
+  LeafTiles cfg;
+  const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m), c0 = a.rows.c0, c1 = a.rows.cend(a.m);
+  if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cfg;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tm_tiles = (r1 - r0 + BM - 1) / BM;
+  auto tiles = [&](int bn) { return tm_tiles * ((c1 - c0 + bn - 1) / bn) * a.n_jobs; };
+  auto waves = [&](int64_t t) { return (double)((t + sms - 1) / sms); };
+  const int64_t t128 = tiles(128);
+  double best = waves(t128);
+  cfg.bn = 128;
+  if (waves(tiles(64)) * 0.5 / 0.98 < best) { best = waves(tiles(64)) * 0.5 / 0.98; cfg.bn = 64; }
+  const int kblocks = (int)((a.m + 31) / 32);
+  // split only where the pieces cannot race another launch on the workspace:
+  // full-width launches (the host pipeline's column regions run on two streams)
+  const bool can_split = !a.post && c0 == 0 && c1 == a.m && kblocks >= 8;
+  const double eps = std::max(0.01, 32.0 / (double)a.m);
+  const int64_t full = t128 / sms;
+  int max_split = 16;
+  if (const char* e = getenv("MF_LEAF_SPLIT")) max_split = std::max(1, atoi(e));
+  for (int64_t w = full; can_split && w >= std::max<int64_t>(0, full - 1); --w) {
+    const int64_t tail = t128 - w * sms;
+    if (tail <= 0) continue;
+    for (int S = 2; S <= max_split && S <= kblocks / 4; ++S) {
+      const double cost = (double)w + waves(tail * S) * (1.0 / S + eps);
+      if (cost < best * 0.995) {
+        best = cost;
+        cfg.bn = 128; cfg.split = S; cfg.n_whole = w * sms; cfg.n_tail = tail;
+      }
+    }
+  }
+  if (const char* e = getenv("MF_LEAF_BN")) {
+    cfg.bn = atoi(e) == 64 ? 64 : 128;
+    if (cfg.bn == 64) cfg.split = 1;
+  }
+  if (cfg.split > 1) cfg.ws_elems = cfg.n_tail * cfg.split * (int64_t)BM * 128;
+  return cfg;
+}
+
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m), c0 = a.rows.c0, c1 = a.rows.cend(a.m);
   if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cudaSuccess;
@@ -490,19 +596,14 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   const bool fuse_ok = !a.post || (!(a.ldo & 1) && al16(a.out));
   if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && fuse_ok && r0 % BM == 0 &&
       c0 % BN == 0 && (c1 == a.m || c1 % BN == 0)) {
-    // Tile width: 64 when 128-wide tiles would leave a badly filled last wave
-    // (e.g. 7 products of 2048^2: 12.1 waves of 148 SMs) -- model: wave fill
-    // times a 2% per-tile penalty for the narrower tile (MF_LEAF_BN overrides).
     const int64_t tm_tiles = (r1 - r0 + BM - 1) / BM;
-    int sms = 148, dev = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    auto fill = [&](int bn) {
-      const double waves = (double)(tm_tiles * ((c1 - c0 + bn - 1) / bn) * a.n_jobs) / sms;
-      return waves / std::ceil(waves);
-    };
-    int bn = fill(64) * 0.98 > fill(128) ? 64 : 128;
-    if (const char* e = getenv("MF_LEAF_BN")) bn = atoi(e) == 64 ? 64 : 128;
+    LeafTiles cfg = leaf_tiles(a);
+    // the caller provides the split-K workspace (run_leaf sizes it from leaf_tiles)
+    if (cfg.split > 1 && (!a.split_ws || a.split_ws_elems < cfg.ws_elems || a.split_cnt_len < cfg.n_tail))
+      cfg.split = 1;
+    const int bn = cfg.bn;
     int ksub = 2;  // k sub-blocks of 16 per pipeline stage
     if (const char* e = getenv("MF_LEAF_KSUB")) ksub = atoi(e) == 1 ? 1 : 2;
     const bool fuse = a.post != nullptr;
@@ -528,9 +629,14 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.jobs = a.jobs;
     prm.post_off = a.post_off;
     prm.post = a.post;
+    prm.split = cfg.split;
+    prm.n_whole = cfg.split > 1 ? (int)cfg.n_whole : 0;
+    prm.part_ws = a.split_ws;
+    prm.part_cnt = a.split_cnt;
     prm.group_m = GROUP_M;
     if (const char* e = getenv("MF_LEAF_GROUPM")) prm.group_m = std::max(1, atoi(e));
-    const int64_t grid = (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
+    const int64_t grid = cfg.split > 1 ? cfg.n_whole + cfg.n_tail * cfg.split
+                                       : (int64_t)prm.tiles_m * prm.tiles_n * a.n_jobs;
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)

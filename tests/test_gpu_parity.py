@@ -496,16 +496,22 @@ def test_host_pipeline_matches_device_path(name, levels, n, path, monkeypatch):
     """mf_dgemm_host's slab pipeline (H2D / K4-K5-K6 per row slab / D2H on
     three streams) computes exactly what mf_dgemm computes: same kernels, same
     per-element order -> bitwise equal on random inputs, exact on integers;
-    host leading dimensions > n are honoured."""
+    host leading dimensions > n are honoured.  (mf_dgemm's own leaf may cut a
+    few-wave launch's tail into split-K pieces, which the pipeline's region
+    launches never do: bitwise with MF_LEAF_SPLIT=1, to rounding otherwise.)"""
     _mix_path(monkeypatch, path)
     t = triples.get(name) if name else None
     A, B = mf_inputs.pair("uniform", n, 15)
     with mf.Plan(t, levels, n) as p:
+        Cs = host(p.dgemm(dev(A), dev(B), alpha=0.75))
+        monkeypatch.setenv("MF_LEAF_SPLIT", "1")
         Cd = host(p.dgemm(dev(A), dev(B), alpha=0.75))
+        monkeypatch.delenv("MF_LEAF_SPLIT")
         Ah = np.zeros((n, n + 8)); Ah[:, :n] = A
         Ch = np.full((n, n + 4), np.nan)
         p.dgemm_host_ptr(Ah.ctypes.data, n + 8, B.ctypes.data, n, Ch.ctypes.data, n + 4, alpha=0.75)
         assert (Ch[:, :n] == Cd).all() and np.isnan(Ch[:, n:]).all()
+        assert scaled(Ch[:, :n], Cs, A, B) <= 1e-14 * max(1, levels)
         Ai, Bi = mf_inputs.pair("int1024", n, 16)
         assert (p.dgemm_host(Ai, Bi) == exact(Ai, Bi)).all()
 
@@ -685,3 +691,30 @@ def test_nccl_rowslab_output_single_rank():
             assert (p.dgemm_host(A, B) == ref).all()
     finally:
         mf.nccl_comm_destroy(comm)
+
+
+# ------------------------------------------------ split-K tail of the leaf launch
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 1, 2048), (SW, 1, 2000), (SW, 1, 4096),
+                                           (None, 0, 2048), ("laderman", 1, 1152)])
+def test_leaf_split_k_tail(name, levels, n, monkeypatch):
+    """Launches that fill the SMs in few waves cut their tail tiles into k-range
+    pieces (mf_leaf.cu leaf_tiles; the last piece sums the partials in split
+    order).  Exact on integers, deterministic (two runs bitwise equal), within
+    the bound on random inputs and close to the unsplit launch (MF_LEAF_SPLIT=1)."""
+    t = triples.get(name) if name else None
+    A, B = mf_inputs.pair("int1024", n, 54)
+    with mf.Plan(t, levels, n) as p:
+        Ad, Bd = dev(A), dev(B)
+        C1 = host(p.dgemm(Ad, Bd))
+        assert (C1 == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 55)
+        Ad, Bd = dev(A), dev(B)
+        Cs = host(p.dgemm(Ad, Bd))
+        assert (host(p.dgemm(Ad, Bd)) == Cs).all()
+    monkeypatch.setenv("MF_LEAF_SPLIT", "1")
+    with mf.Plan(t, levels, n) as p:
+        Cn = host(p.dgemm(Ad, Bd))
+    Cref = oracle.classical(A, B)
+    assert scaled(Cs, Cref, A, B) <= 1e-13 * max(1, levels)
+    assert scaled(Cs, Cn, A, B) <= 1e-14 * max(1, levels)
