@@ -442,15 +442,15 @@ def main():
         out["max_scaled_error"] = err / den
         out["error_bound"] = 1e-13 * max(1, a.levels)
         if not a.no_classical and world == 1:
-            def timeit(fn):
+            def timeit(fn, st=stream):
                 for _ in range(2):
                     fn()
                 torch.cuda.synchronize()
                 s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
+                s0.record(st)
                 for _ in range(a.steps):
                     fn()
-                s1.record(stream)
+                s1.record(st)
                 torch.cuda.synchronize()
                 return s0.elapsed_time(s1) / a.steps
             t_cublas = timeit(lambda: torch.matmul(A, B, out=Cref))
@@ -460,6 +460,15 @@ def main():
             out["classical"] = {"cublas_dgemm_tflops": fl / (t_cublas * 1e-3), "cublas_ms": t_cublas,
                                 "mf_levels0_tflops": fl / (t_leaf0 * 1e-3), "mf_levels0_ms": t_leaf0}
             out["speedup_vs_cublas"] = t_cublas / ms
+            if n <= 4096:  # launch-bound sizes: the same step replayed as a CUDA graph
+                gs = torch.cuda.Stream()
+                with mf.Plan(triple, a.levels, n, device=local, graph=True,
+                             level_by_level=a.level_by_level, recurse_levels=a.recurse_levels,
+                             fuse_postadd=a.fuse, leaf=a.leaf) as pg, torch.cuda.stream(gs):
+                    t_graph = timeit(lambda: pg.dgemm(A, B, C, stream=gs), gs)
+                out["graph"] = {"ms_per_step": t_graph, "value": fl / (t_graph * 1e-3), "unit": UNIT,
+                                "what": "mf_options.graph: the same launches replayed as one "
+                                        "CUDA graph per step (no profiling events)"}
         del Cref
 
     # ---- end to end through the C ABI with host buffers (every rank: its

@@ -108,6 +108,16 @@ typedef struct {
                            level_by_level) and no batching, else
                            MF_ERR_UNSUPPORTED.  Odd ldc or C not 16-byte aligned
                            run the simple leaf with f64 atomics instead       */
+  int32_t graph;          /* 1: mf_dgemm replays a CUDA graph of its launches.  The
+                           first call with a given (A, lda, B, ldb, C, ldc,
+                           alpha) runs eagerly; the second captures the step
+                           on the call's stream and instantiates it; later
+                           calls with the same arguments launch the graph (one
+                           host call instead of four launches: the n <= 4096
+                           configs are host-issue bound).  Ignored on the
+                           legacy default stream (NULL) and with profile,
+                           nccl_comm, level_by_level or MF_LEAF_CUBLAS      */
+  int32_t reserved0;      /* must be 0                                            */
   int32_t recurse_levels; /* with level_by_level = 1: how many top levels run one
                            at a time (0 = levels - 1, the paper's full
                            recursion); the remaining levels run as ONE

@@ -50,7 +50,8 @@ class mf_options(ctypes.Structure):
                 ("input_mode", ctypes.c_int32), ("output_mode", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("host_only", ctypes.c_int32),
                 ("level_by_level", ctypes.c_int32), ("max_workspace", ctypes.c_int64),
-                ("fuse_postadd", ctypes.c_int32), ("recurse_levels", ctypes.c_int32)]
+                ("fuse_postadd", ctypes.c_int32), ("graph", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32), ("recurse_levels", ctypes.c_int32)]
 
 
 _P, _D, _I32, _I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64
@@ -120,7 +121,8 @@ class Plan:
                  device: int | None = None, shard_rank: int = 0, shard_count: int = 1,
                  nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT,
                  profile: bool = False, host_only: bool = False, level_by_level: bool = False,
-                 max_workspace: int = 0, fuse_postadd: bool = False, recurse_levels: int = 0):
+                 max_workspace: int = 0, fuse_postadd: bool = False, recurse_levels: int = 0,
+                 graph: bool = False):
         self.triple, self.levels, self.n = triple, int(levels), int(n)
         opt = mf_options()
         opt.struct_size = ctypes.sizeof(mf_options)
@@ -135,6 +137,7 @@ class Plan:
         opt.max_workspace = int(max_workspace)
         opt.fuse_postadd = int(bool(fuse_postadd))
         opt.recurse_levels = int(recurse_levels)
+        opt.graph = int(bool(graph))
         self._opt = opt
         h = ctypes.c_void_p()
         if triple is None:

@@ -261,6 +261,7 @@ void free_plan(Plan* pl) {
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
   if (pl->cublas) cublas()->Destroy(pl->cublas);
+  if (pl->g_exec) cudaGraphExecDestroy(pl->g_exec);
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
@@ -445,6 +446,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
                 (long long)n, o.shard_count);
   if (o.fuse_postadd && o.leaf == MF_LEAF_CUBLAS)
     return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs the DMMA or simple leaf");
+  if (o.reserved0 != 0) return fail(MF_ERR_INVALID_ARG, "mf_options.reserved0 must be 0");
   if (o.recurse_levels < 0)
     return fail(MF_ERR_INVALID_ARG, "recurse_levels must be >= 0 (got %d)", o.recurse_levels);
   if (o.fuse_postadd && levels < 1)
@@ -476,6 +478,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     mf_options top = o, sub = o;
     top.level_by_level = 0;
     top.recurse_levels = 0;
+    sub.graph = 0;
     sub.level_by_level = r > 1 ? 1 : 0;
     sub.recurse_levels = r > 1 ? r - 1 : 0;
     sub.shard_rank = 0; sub.shard_count = 1; sub.nccl_comm = nullptr; sub.profile = 0;
@@ -825,8 +828,55 @@ static mf_status check_mat(const char* name, const void* X, int64_t ld, int64_t 
   return MF_OK;
 }
 
+static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_t lda,
+                             const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+
+// mf_options.graph: eager on the first call with an argument tuple, captured on
+// the second (every allocation and attribute set-up already happened), replayed
+// from then on.  The graph holds the same launches with the same parameters.
 mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double* C, int64_t ldc, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!pl || !pl->opt.graph || pl->opt.profile || pl->opt.host_only || pl->nccl_comm || pl->child ||
+      pl->leaf == MF_LEAF_CUBLAS || s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread)
+    return dgemm_eager(pl, alpha, A, lda, B, ldb, C, ldc, stream);
+  Plan::GraphKey key;
+  key.A = A; key.B = B; key.C = C; key.lda = lda; key.ldb = ldb; key.ldc = ldc; key.alpha = alpha;
+  DeviceGuard guard(pl->device);
+  if (pl->g_exec && pl->g_key == key) {
+    g_err.clear();
+    MF_CUDA(cudaGraphLaunch(pl->g_exec, s), "cudaGraphLaunch");
+    return MF_OK;
+  }
+  if (!(pl->g_has_seen && pl->g_seen == key)) {
+    pl->g_seen = key;
+    pl->g_has_seen = true;
+    return dgemm_eager(pl, alpha, A, lda, B, ldb, C, ldc, stream);
+  }
+  MF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  mf_status st = dgemm_eager(pl, alpha, A, lda, B, ldb, C, ldc, stream);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+  if (st != MF_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ce != cudaSuccess || !graph)
+    return fail(MF_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+  if (pl->g_exec) { cudaGraphExecDestroy(pl->g_exec); pl->g_exec = nullptr; }
+  const cudaError_t ie = cudaGraphInstantiate(&pl->g_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    pl->g_exec = nullptr;
+    return fail(MF_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ie));
+  }
+  pl->g_key = key;
+  MF_CUDA(cudaGraphLaunch(pl->g_exec, s), "cudaGraphLaunch");
+  return MF_OK;
+}
+
+static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_t lda,
+                             const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
   g_err.clear();
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");

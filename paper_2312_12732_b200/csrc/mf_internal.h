@@ -125,6 +125,20 @@ struct Plan {
   const double** d_ptrs = nullptr;  // device pointer arrays for cublasDgemmBatched
   size_t d_ptrs_cap = 0;
   double* Cfull = nullptr;      // MF_OUT_ROWSLAB: the full partial C before reduce-scatter
+  // mf_options.graph: the step as an instantiated CUDA graph for one argument tuple
+  struct GraphKey {
+    const double *A = nullptr, *B = nullptr;
+    double* C = nullptr;
+    int64_t lda = 0, ldb = 0, ldc = 0;
+    double alpha = 0.0;
+    bool operator==(const GraphKey& o) const {
+      return A == o.A && B == o.B && C == o.C && lda == o.lda && ldb == o.ldb && ldc == o.ldc &&
+             alpha == o.alpha;
+    }
+  };
+  GraphKey g_key, g_seen;       // key of g_exec; key of the last eager call
+  bool g_has_seen = false;
+  cudaGraphExec_t g_exec = nullptr;
   double* split_ws = nullptr;   // leaf split-K tail: partial tiles (grown on demand)
   int64_t split_ws_elems = 0;
   int* split_cnt = nullptr;     // ... and arrival counters (zeroed at allocation)

@@ -718,3 +718,34 @@ def test_leaf_split_k_tail(name, levels, n, monkeypatch):
     Cref = oracle.classical(A, B)
     assert scaled(Cs, Cref, A, B) <= 1e-13 * max(1, levels)
     assert scaled(Cs, Cn, A, B) <= 1e-14 * max(1, levels)
+
+
+# ------------------------------------------------ CUDA-graph replay of the step
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 1, 64), (SW, 2, 512), (SW, 1, 2048), (None, 0, 256),
+                                           ("laderman", 1, 390)])
+def test_graph_replay_matches_eager(name, levels, n):
+    """mf_options.graph: call 1 eager, call 2 captured + launched, calls 3+
+    replayed -- all bitwise the eager result (the same launches); new
+    arguments re-capture; the legacy default stream stays eager."""
+    t = triples.get(name) if name else None
+    A, B = mf_inputs.pair("uniform", n, 56)
+    Ad, Bd = dev(A), dev(B)
+    with mf.Plan(t, levels, n) as p:
+        ref = host(p.dgemm(Ad, Bd, alpha=0.5))
+    side = torch.cuda.Stream()
+    with mf.Plan(t, levels, n, graph=True) as p:
+        C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        with torch.cuda.stream(side):
+            for _ in range(4):
+                C.fill_(float("nan"))
+                p.dgemm(Ad, Bd, C=C, alpha=0.5, stream=side)
+                side.synchronize()
+                assert (host(C) == ref).all()
+            C2 = torch.empty_like(C)
+            for _ in range(3):  # new output pointer and alpha: eager, capture, replay
+                p.dgemm(Ad, Bd, C=C2, alpha=1.0, stream=side)
+            side.synchronize()
+        assert (host(C2) == 2.0 * ref).all()
+        p.dgemm(Ad, Bd, C=C2, alpha=0.5)  # legacy stream: eager path
+        assert (host(C2) == ref).all()
