@@ -68,9 +68,12 @@ CONFIGS = {
     # flattened SW^3 child plan (343 leaves in one launch); mf_options.recurse_levels
     "x-sw4-16384-hybrid": (16384, "strassen-winograd", 4),
     "x-sw4-32768-hybrid": (32768, "strassen-winograd", 4),
+    # five levels at n=32768: two levels one at a time (49 products), each a
+    # flattened SW^3 child at n=8192 (m = 1024)
+    "x-sw5-32768-hybrid": (32768, "strassen-winograd", 5),
 }
 # presets run level by level with this many recursive top levels
-PRESET_RECURSE = {"x-sw4-16384-hybrid": 1, "x-sw4-32768-hybrid": 1}
+PRESET_RECURSE = {"x-sw4-16384-hybrid": 1, "x-sw4-32768-hybrid": 1, "x-sw5-32768-hybrid": 2}
 # presets that need a workspace cap (GB): 49152^2 * 8 B = 19.3 GB per matrix;
 # all 129 T/S/P blocks (1.2 GB each) would need 156 GB on top of A, B, C, C_ref
 PRESET_WORKSPACE_GB = {"x-sw2-49152-bounded": 85.0}
