@@ -112,6 +112,9 @@ def parse():
                          "last); the rest run as one flattened child plan")
     ap.add_argument("--leaf", choices=["dmma", "cublas", "simple"], default="dmma",
                     help="leaf GEMM: our TMA+DMMA kernel (default) or the cuBLAS ablation")
+    ap.add_argument("--comm-regions", type=int, default=0,
+                    help="sharded runs: row regions whose C rows are reduced while the next "
+                         "region computes (0 = library default)")
     ap.add_argument("--fuse", action="store_true",
                     help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd)")
     a = ap.parse_args()
@@ -371,7 +374,7 @@ def main():
     plan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
                    nccl_comm=comm, profile=True, level_by_level=a.level_by_level,
                    max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse,
-                   recurse_levels=a.recurse_levels, leaf=a.leaf)
+                   recurse_levels=a.recurse_levels, leaf=a.leaf, comm_regions=a.comm_regions)
     info = plan.info()
     stream = torch.cuda.current_stream()
     A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")

@@ -117,7 +117,15 @@ typedef struct {
                            configs are host-issue bound).  Ignored on the
                            legacy default stream (NULL) and with profile,
                            nccl_comm, level_by_level or MF_LEAF_CUBLAS      */
-  int32_t reserved0;      /* must be 0                                            */
+  int32_t comm_regions;   /* sharded plans with nccl_comm (MF_OUT_ROOT / _ALL): the
+                           leaf and post-addition run in this many 128-aligned
+                           row regions, and each region's rows of C are reduced
+                           on a separate stream while the next region computes
+                           ("reduce C block-groups as
+                           products complete").  0 = default (8 when
+                           shard_count > 1, else 1); 1 = one reduce after K6.
+                           Without nccl_comm an explicit value > 1 still runs
+                           the regions (the shard's partial C; for tests)    */
   int32_t recurse_levels; /* with level_by_level = 1: how many top levels run one
                            at a time (0 = levels - 1, the paper's full
                            recursion); the remaining levels run as ONE

@@ -51,7 +51,7 @@ class mf_options(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("host_only", ctypes.c_int32),
                 ("level_by_level", ctypes.c_int32), ("max_workspace", ctypes.c_int64),
                 ("fuse_postadd", ctypes.c_int32), ("graph", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32), ("recurse_levels", ctypes.c_int32)]
+                ("comm_regions", ctypes.c_int32), ("recurse_levels", ctypes.c_int32)]
 
 
 _P, _D, _I32, _I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64
@@ -122,7 +122,7 @@ class Plan:
                  nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT,
                  profile: bool = False, host_only: bool = False, level_by_level: bool = False,
                  max_workspace: int = 0, fuse_postadd: bool = False, recurse_levels: int = 0,
-                 graph: bool = False):
+                 graph: bool = False, comm_regions: int = 0):
         self.triple, self.levels, self.n = triple, int(levels), int(n)
         opt = mf_options()
         opt.struct_size = ctypes.sizeof(mf_options)
@@ -138,6 +138,7 @@ class Plan:
         opt.fuse_postadd = int(bool(fuse_postadd))
         opt.recurse_levels = int(recurse_levels)
         opt.graph = int(bool(graph))
+        opt.comm_regions = int(comm_regions)
         self._opt = opt
         h = ctypes.c_void_p()
         if triple is None:

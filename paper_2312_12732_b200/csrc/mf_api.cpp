@@ -265,10 +265,11 @@ void free_plan(Plan* pl) {
   for (auto& set : pl->prof_events)
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : pl->comm_events) cudaEventDestroy(e);
   for (auto& b : pl->batches)
     for (void* p : {b.mixA.d_table, b.mixB.d_table, b.mixC.d_table})
       if (p) cudaFree(p);
-  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
+  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm})
     if (st) cudaStreamDestroy(st);
 }
 
@@ -446,7 +447,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
                 (long long)n, o.shard_count);
   if (o.fuse_postadd && o.leaf == MF_LEAF_CUBLAS)
     return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs the DMMA or simple leaf");
-  if (o.reserved0 != 0) return fail(MF_ERR_INVALID_ARG, "mf_options.reserved0 must be 0");
+  if (o.comm_regions < 0)
+    return fail(MF_ERR_INVALID_ARG, "comm_regions must be >= 0 (got %d)", o.comm_regions);
   if (o.recurse_levels < 0)
     return fail(MF_ERR_INVALID_ARG, "recurse_levels must be >= 0 (got %d)", o.recurse_levels);
   if (o.fuse_postadd && levels < 1)
@@ -830,6 +832,19 @@ static mf_status check_mat(const char* name, const void* X, int64_t ld, int64_t 
 
 static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_t lda,
                              const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n);
+
+// Row regions of the region-overlapped exchange (mf_options.comm_regions).
+// Without nccl_comm only an explicit comm_regions > 1 applies (the regions
+// are computed, nothing is reduced: the emulated ranks' partial C, for tests).
+static int comm_regions(const Plan& pl) {
+  if ((pl.nccl_comm && pl.opt.output_mode == MF_OUT_ROWSLAB) || pl.child || pl.fuse ||
+      !pl.batches.empty() || pl.levels == 0 || (!pl.nccl_comm && pl.opt.comm_regions <= 1))
+    return 1;
+  const int want = pl.opt.comm_regions > 0 ? pl.opt.comm_regions
+                                           : (pl.nccl_comm && pl.shard_count > 1 ? 8 : 1);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (pl.m + 127) / 128));
+}
 
 // mf_options.graph: eager on the first call with an argument tuple, captured on
 // the second (every allocation and attribute set-up already happened), replayed
@@ -930,6 +945,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
 
   cudaEvent_t* ev = prof_slot(pl);
   if (pl->opt.profile) ++pl->prof_calls;
+  bool reduced = false;  // C already summed over ranks region by region
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
   mark(0);
   if (pl->levels == 0) {
@@ -1007,6 +1023,74 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
                            pl->Pw + (int64_t)q * mm, m, stream)) != MF_OK)
           return st;
       }
+    } else if (comm_regions(*pl) > 1) {
+      // a3 + a4 + a6 by row regions (NEXT-4): region k's leaf products and
+      // post-addition, then its rows of the partial C (one contiguous piece per
+      // block row) are reduced on pl->comm while region k+1 computes.  Every
+      // rank issues the same collectives in the same order.
+      const int K = comm_regions(*pl);
+      if (pl->nccl_comm && ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");
+      if (!pl->comm) MF_CUDA(cudaStreamCreateWithFlags(&pl->comm, cudaStreamNonBlocking), "stream");
+      while ((int)pl->comm_events.size() < K + 1) {
+        cudaEvent_t e;
+        MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        pl->comm_events.push_back(e);
+      }
+      ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
+      const bool exchange = comm != nullptr;
+      const int64_t m = pl->m;
+      auto post = [&](int64_t a, int64_t b, const MixTable& t) -> mf_status {
+        if (a >= b) return MF_OK;
+        Rows q;
+        q.r0 = a; q.r1 = b;
+        MF_CUDA(launch_postmix(*pl, t, alpha, pl->Pw, C, ldc, s, q), "post-add (K6, region)");
+        return MF_OK;
+      };
+      MF_CUDA(cudaEventRecord(pl->comm_events[K], s), "event");
+      MF_CUDA(cudaStreamWaitEvent(pl->comm, pl->comm_events[K], 0), "wait");  // comm after K4
+      for (int k = 0; k < K; ++k) {
+        const auto rg = tile_piece(m, k, K);
+        if (rg.second <= rg.first) continue;
+        Rows r;
+        r.r0 = rg.first; r.r1 = rg.second;
+        if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, r)) != MF_OK)
+          return st;
+        if (!pl->my_part.empty()) {
+          Rows pr;
+          pr.r0 = std::max<int64_t>(rg.first, pl->part_r0);
+          pr.r1 = std::min<int64_t>(rg.second, pl->part_r1);
+          if (pr.r0 < pr.r1 &&
+              (st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, pr, true)) != MF_OK)
+            return st;
+          if ((st = post(rg.first, std::min<int64_t>(rg.second, pl->part_r0), pl->mixC)) != MF_OK ||
+              (st = post(std::max<int64_t>(rg.first, pl->part_r0), std::min<int64_t>(rg.second, pl->part_r1),
+                         pl->mixC2)) != MF_OK ||
+              (st = post(std::max<int64_t>(rg.first, pl->part_r1), rg.second, pl->mixC)) != MF_OK)
+            return st;
+        } else if ((st = post(rg.first, rg.second, pl->mixC)) != MF_OK) {
+          return st;
+        }
+        if (!exchange) continue;
+        MF_CUDA(cudaEventRecord(pl->comm_events[k], s), "event");
+        MF_CUDA(cudaStreamWaitEvent(pl->comm, pl->comm_events[k], 0), "wait");
+        const size_t count = (size_t)(rg.second - rg.first) * n;
+        nc->GroupStart();
+        for (int br = 0; br < pl->P; ++br) {
+          double* piece = C + (br * m + rg.first) * n;
+          ncclResult_t rr = pl->opt.output_mode == MF_OUT_ALL
+                                ? nc->AllReduce(piece, piece, count, ncclDouble, ncclSum, comm, pl->comm)
+                                : nc->Reduce(piece, piece, count, ncclDouble, ncclSum, 0, comm, pl->comm);
+          if (rr != ncclSuccess) {
+            nc->GroupEnd();
+            return nccl_fail(nc, rr, "ncclReduce(C region)");
+          }
+        }
+        ncclResult_t rr = nc->GroupEnd();
+        if (rr != ncclSuccess) return nccl_fail(nc, rr, "ncclGroupEnd");
+      }
+      MF_CUDA(cudaEventRecord(pl->comm_events[K], pl->comm), "event");
+      MF_CUDA(cudaStreamWaitEvent(s, pl->comm_events[K], 0), "wait");
+      reduced = true;  // (without a communicator: the region K6 wrote the partial C)
     } else {
       // a3: all leaf products in one launch (K5); split products on this rank's slab
       if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) !=
@@ -1022,7 +1106,9 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     }
     mark(3);
     // a4: fused post-addition (K6); rows holding split-product slabs use mixC2
-    if (pl->my_part.empty()) {
+    if (reduced) {
+      // done region by region above
+    } else if (pl->my_part.empty()) {
       MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, pl->Pw, C, ldc, s), "post-add (K6)");
     } else {
       Rows lo, mid, hi;
@@ -1035,7 +1121,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     }
   }
   mark(4);
-  if (pl->nccl_comm) {
+  if (pl->nccl_comm && !reduced) {
     // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
     ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
     if (ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");

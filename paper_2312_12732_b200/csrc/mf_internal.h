@@ -154,6 +154,8 @@ struct Plan {
   Plan* child = nullptr;
   // host-buffer pipeline (mf_dgemm_host): copy streams and per-slab events
   cudaStream_t h2d = nullptr, d2h = nullptr, mixs = nullptr, s2 = nullptr;
+  cudaStream_t comm = nullptr;   // region-overlapped NCCL reduces (comm_regions > 1)
+  std::vector<cudaEvent_t> comm_events;
   std::vector<cudaEvent_t> pipe_events;
   // phase profiling (mf_options.profile): 6 events per mf_dgemm call
   std::vector<std::vector<cudaEvent_t>> prof_events;

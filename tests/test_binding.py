@@ -177,6 +177,8 @@ def test_fused_postadd_option_validation():
     st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, level_by_level=1, recurse_levels=-1,
                            host_only=1)
     assert st == mf.MF_ERR_INVALID_ARG and "recurse_levels" in msg
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, comm_regions=-2, host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "comm_regions" in msg
     p = mf.Plan(t, 2, 64, fuse_postadd=True, host_only=True)
     assert p.info()["n_products"] == 49
     p.close()

@@ -749,3 +749,57 @@ def test_graph_replay_matches_eager(name, levels, n):
         assert (host(C2) == 2.0 * ref).all()
         p.dgemm(Ad, Bd, C=C2, alpha=0.5)  # legacy stream: eager path
         assert (host(C2) == ref).all()
+
+
+
+# ------------------------------------------------ region-overlapped exchange (NEXT-4)
+
+@pytest.mark.parametrize("N", [1, 3, 8])
+def test_comm_regions_partials_match_one_shot(N, monkeypatch):
+    """comm_regions: the leaf and K6 by 128-aligned row regions (each region's C
+    rows reduced while the next computes).  Without a communicator the shard's
+    partial C is returned: bitwise the one-shot partial (same launches per
+    element; split-K off on both sides), whole and split products alike; the
+    N partials sum to the exact product on integers."""
+    monkeypatch.setenv("MF_LEAF_SPLIT", "1")
+    n = 2048
+    A, B = mf_inputs.pair("int1024", n, 57)
+    Ad, Bd = dev(A), dev(B)
+    total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    U, V = mf_inputs.pair("uniform", n, 58)
+    Ud, Vd = dev(U), dev(V)
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N, comm_regions=4) as p:
+            total += p.dgemm(Ad, Bd)
+            Cr = host(p.dgemm(Ud, Vd, alpha=0.5))
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N) as p:
+            assert (host(p.dgemm(Ud, Vd, alpha=0.5)) == Cr).all()
+    assert (host(total) == exact(A, B)).all()
+
+
+def test_comm_regions_nccl_single_rank(monkeypatch):
+    """The region-overlapped NCCL exchange on a 1-rank communicator (reduce and
+    all-reduce of each region's C rows on the comm stream): bitwise the local
+    result with split-K off, within rounding with it on."""
+    n = 1024
+    A, B = mf_inputs.pair("uniform", n, 59)
+    Ad, Bd = dev(A), dev(B)
+    comm = mf.nccl_comm_create(mf.nccl_unique_id(), 0, 1)
+    try:
+        for split in ("1", None):
+            if split:
+                monkeypatch.setenv("MF_LEAF_SPLIT", split)
+            else:
+                monkeypatch.delenv("MF_LEAF_SPLIT", raising=False)
+            with mf.Plan(triples.get(SW), 2, n) as p:
+                ref = host(p.dgemm(Ad, Bd))
+            for out_mode in (mf.OUT_ROOT, mf.OUT_ALL):
+                with mf.Plan(triples.get(SW), 2, n, shard_rank=0, shard_count=1, nccl_comm=comm,
+                             output_mode=out_mode, input_mode=mf.IN_REPLICATED, comm_regions=8) as p:
+                    C = host(p.dgemm(Ad, Bd))
+                if split:
+                    assert (C == ref).all()
+                else:
+                    assert scaled(C, ref, A, B) <= 1e-14
+    finally:
+        mf.nccl_comm_destroy(comm)
