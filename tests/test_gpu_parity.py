@@ -803,3 +803,21 @@ def test_comm_regions_nccl_single_rank(monkeypatch):
                     assert scaled(C, ref, A, B) <= 1e-14
     finally:
         mf.nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("regions", [0, 4])
+def test_three_level_sharding_n8(regions):
+    """NEXT-4 three-level sharding: SW^3's 343 products over 8 ranks (343 =
+    8*42 + 7: 42 whole products each plus a 128-row slab of each of the 7
+    leftovers), emulated on one GPU, with and without row regions.  The 8
+    partial C sum to A*B: exact Freivalds on integers."""
+    n, N = 8192, 8
+    Ad, Bd = mf_inputs.device_pair("int1024", n, 60)
+    total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 3, n, shard_rank=r, shard_count=N, comm_regions=regions) as p:
+            pr = p.products()["shard"]
+            assert (pr == r).sum() == 42 and (pr == -1).sum() == 7
+            total += p.dgemm(Ad, Bd)
+    A, B, C = host(Ad), host(Bd), host(total)
+    assert oracle.freivalds_int(A, B, C, trials=2) == 0
