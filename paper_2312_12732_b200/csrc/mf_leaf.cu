@@ -546,7 +546,9 @@ bool leaf_tma_supported(const LeafArgs& a) {
 //    per-piece overhead (prologue + partial store/reload, ~4 us against a
 //    0.13 us-per-k tile).
 // E.g. 7 products of 2048^2 (config 2): 1792 tiles = 12.1 waves -> 12 whole
-// waves + 16 tiles x 9 pieces (12.13) instead of 25 half-width waves (12.76).
+// waves + 16 tiles x 9 pieces (12.13) instead of 25 half-width waves (12.76);
+// 49 products of 4096^2: 339 whole waves + the 4 leftover tiles as 16 pieces
+// each (339.07 instead of 340).
 // MF_LEAF_BN / MF_LEAF_SPLIT override.
 LeafTiles leaf_tiles(const LeafArgs& a) {
   LeafTiles cfg;
@@ -575,7 +577,7 @@ LeafTiles leaf_tiles(const LeafArgs& a) {
     if (tail <= 0) continue;
     for (int S = 2; S <= max_split && S <= kblocks / 4; ++S) {
       const double cost = (double)w + waves(tail * S) * (1.0 / S + eps);
-      if (cost < best * 0.995) {
+      if (cost < best - 0.02) {  // worth at least 2% of one tile's time
         best = cost;
         cfg.bn = 128; cfg.split = S; cfg.n_whole = w * sms; cfg.n_tail = tail;
       }
