@@ -486,20 +486,34 @@ def main():
         Ah.copy_(A); Bh.copy_(B)
         del A, B, C
         torch.cuda.empty_cache()
-        plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)  # warm-up
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(a.steps):
-            plan.dgemm_host_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)
-        dt = (time.perf_counter() - t0) / a.steps
-        if distributed:
-            t = torch.tensor([dt], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        args = (Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n)
+
+        def e2e_time(call, sync):
+            call(*args)  # warm-up
+            sync()
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(a.steps):
+                call(*args)
+            sync()
+            dt = (time.perf_counter() - t0) / a.steps
+            if distributed:
+                t = torch.tensor([dt], device=dev, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = float(t.item())
+            return dt
+        # a stream of K products through mf_dgemm_host_async (call k+1's copies
+        # under call k's compute), and single synchronous calls
+        dt = e2e_time(plan.dgemm_host_async_ptr, plan.host_sync)
+        dts = e2e_time(plan.dgemm_host_ptr, lambda: None)
         out["e2e"] = {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "ms_per_step": dt * 1e3,
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
-                      "api": "mf_dgemm_host (pinned host A, B, C; H2D + compute + D2H per step"
-                             + (", per rank, NCCL reduce inside)" if distributed else ")")}
+                      "api": "mf_dgemm_host_async x K steps + mf_host_sync (pinned host A, B, C; "
+                             "every step's H2D + compute + D2H inside the timed region; consecutive "
+                             "steps overlap copies with compute"
+                             + (", per rank, NCCL reduce inside)" if distributed else ")"),
+                      "sync": {"value": 2.0 * n ** 3 / dts / 1e12, "ms_per_step": dts * 1e3,
+                               "api": "mf_dgemm_host: one synchronous call per step"}}
         out["gpu_launches_e2e_per_step"] = launches_per_step(a)
 
     # ---- variants at the same n, same run: one more recursion level (deeper

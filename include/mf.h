@@ -173,6 +173,24 @@ mf_status mf_dgemm(mf_plan_t plan, double alpha, const double* A, int64_t lda,
 mf_status mf_dgemm_host(mf_plan_t plan, double alpha, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
+/* mf_dgemm_host_async -- mf_dgemm_host without the final wait, for a stream of
+ * products: consecutive calls alternate between two plan-owned device copies
+ * of A, B, C, so call k+1's host->device copies run while call k computes and
+ * call k's device->host copies run while call k+1 computes (the leaf/K6
+ * workspace is shared, so computations stay in call order).  Results are
+ * bitwise those of mf_dgemm_host.  A and B must stay unchanged and C unread
+ * until mf_host_sync (or a synchronisation of `stream`, which waits for the
+ * call's last copy) returns; pinned host memory is needed for the overlap.
+ * Plans without the region pipeline (sharded, NCCL, level-by-level, batched,
+ * fused, non-DMMA leaf) run the call synchronously.  A later synchronous call
+ * on the plan first waits for all enqueued async calls. */
+mf_status mf_dgemm_host_async(mf_plan_t plan, double alpha, const double* A, int64_t lda,
+                              const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* mf_host_sync -- wait until every mf_dgemm_host_async call enqueued on the
+ * plan has finished (its C is on the host). */
+mf_status mf_host_sync(mf_plan_t plan);
+
 /* mf_destroy -- wait for the plan's outstanding work, free it.  NULL: no-op. */
 mf_status mf_destroy(mf_plan_t plan);
 

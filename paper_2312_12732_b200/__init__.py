@@ -40,7 +40,7 @@ OUT_ROOT, OUT_ALL, OUT_ROWSLAB = 0, 1, 2
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
            "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
-           "mf_plan_shard_rows")
+           "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync")
 
 
 class mf_options(ctypes.Structure):
@@ -59,6 +59,8 @@ _lib.mf_plan.argtypes = [ctypes.POINTER(_P), _I32, _I32, _P, _P, _P, _I32, _I64,
                          ctypes.POINTER(mf_options)]
 _lib.mf_dgemm.argtypes = [_P, _D, _P, _I64, _P, _I64, _P, _I64, _P]
 _lib.mf_dgemm_host.argtypes = [_P, _D, _P, _I64, _P, _I64, _P, _I64, _P]
+_lib.mf_dgemm_host_async.argtypes = [_P, _D, _P, _I64, _P, _I64, _P, _I64, _P]
+_lib.mf_host_sync.argtypes = [_P]
 _lib.mf_destroy.argtypes = [_P]
 _lib.mf_last_error.argtypes = []
 _lib.mf_last_error.restype = ctypes.c_char_p
@@ -230,6 +232,17 @@ class Plan:
         """mf_dgemm_host on raw host pointers (e.g. pinned torch CPU tensors)."""
         _check(_lib.mf_dgemm_host(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
                                   _stream_ptr(stream)))
+
+    def dgemm_host_async_ptr(self, pa: int, lda: int, pb: int, ldb: int, pc: int, ldc: int,
+                             alpha: float = 1.0, stream=None):
+        """mf_dgemm_host_async on raw host pointers: enqueue, return at once; the
+        host buffers must stay untouched (A, B) / unread (C) until host_sync()."""
+        _check(_lib.mf_dgemm_host_async(self._h, float(alpha), pa, lda, pb, ldb, pc, ldc,
+                                        _stream_ptr(stream)))
+
+    def host_sync(self):
+        """mf_host_sync: wait for every enqueued dgemm_host_async call."""
+        _check(_lib.mf_host_sync(self._h))
 
     # -- the steps, for step-by-step parity tests -------------------------------
     def premix(self, side: str, X, out, stream=None):

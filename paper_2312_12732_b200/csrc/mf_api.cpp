@@ -256,7 +256,8 @@ void free_plan(Plan* pl) {
                   (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
-                  (void*)pl->split_ws, (void*)pl->split_cnt,
+                  (void*)pl->split_ws, (void*)pl->split_cnt, (void*)pl->hA2, (void*)pl->hB2,
+                  (void*)pl->hC2,
                   (void*)pl->hC})
     if (p) cudaFree(p);
   if (pl->done) cudaEventDestroy(pl->done);
@@ -266,10 +267,12 @@ void free_plan(Plan* pl) {
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->comm_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : {pl->set_free[0], pl->set_free[1], pl->compute_done})
+    if (e) cudaEventDestroy(e);
   for (auto& b : pl->batches)
     for (void* p : {b.mixA.d_table, b.mixB.d_table, b.mixC.d_table})
       if (p) cudaFree(p);
-  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm})
+  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm, pl->cs1})
     if (st) cudaStreamDestroy(st);
 }
 
@@ -1177,7 +1180,9 @@ static int pipeline_slabs(const Plan& pl) {
       !pl.batches.empty() || pl.fuse)
     return 1;
   const int64_t tiles = (pl.m + 127) / 128;
-  return (int)std::min<int64_t>(8, tiles);
+  int want = 8;
+  if (const char* e = getenv("MF_HOST_SLABS")) want = std::max(2, atoi(e));
+  return (int)std::min<int64_t>(want, tiles);
 }
 
 // piece i of n over the 128-aligned tiles of [0, m)
@@ -1186,8 +1191,42 @@ static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n) {
   return {std::min<int64_t>(m, 128 * (i * tiles / n)), std::min<int64_t>(m, 128 * ((i + 1) * tiles / n))};
 }
 
+// Wait for every enqueued mf_dgemm_host_async call of the plan.
+static mf_status host_drain(Plan* pl) {
+  for (int b = 0; b < 2; ++b)
+    if (pl->set_busy[b]) {
+      MF_CUDA(cudaEventSynchronize(pl->set_free[b]), "cudaEventSynchronize");
+      pl->set_busy[b] = false;
+    }
+  pl->compute_pending = false;
+  return MF_OK;
+}
+
+static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t lda,
+                           const double* B, int64_t ldb, double* C, int64_t ldc, void* stream,
+                           bool async);
+
 mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* C, int64_t ldc, void* stream) {
+  return host_call(pl, alpha, A, lda, B, ldb, C, ldc, stream, false);
+}
+
+mf_status mf_dgemm_host_async(mf_plan_t pl, double alpha, const double* A, int64_t lda,
+                              const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
+  return host_call(pl, alpha, A, lda, B, ldb, C, ldc, stream, true);
+}
+
+mf_status mf_host_sync(mf_plan_t pl) {
+  g_err.clear();
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  if (pl->opt.host_only) return MF_OK;
+  DeviceGuard guard(pl->device);
+  return host_drain(pl);
+}
+
+static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t lda,
+                           const double* B, int64_t ldb, double* C, int64_t ldc, void* stream,
+                           bool async) {
   g_err.clear();
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
@@ -1203,6 +1242,9 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B");
   if (!pl->hC && cudaMalloc(&pl->hC, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C");
   const int ns = pipeline_slabs(*pl);
+  // synchronous calls (and plans without the region pipeline) first finish
+  // every enqueued async call
+  if ((!async || ns <= 1) && (st = host_drain(pl)) != MF_OK) return st;
   if (ns <= 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
     MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
     MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
@@ -1220,6 +1262,23 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   const int64_t m = pl->m;
   const int P = pl->P;
   const int nc = ns;  // square grid of regions
+  // async calls alternate between two device sets so call k+1's inputs
+  // stream in while call k computes
+  const int set = async ? (int)(pl->async_calls & 1) : 0;
+  if (set == 1) {
+    if (!pl->hA2 && cudaMalloc(&pl->hA2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device A (2nd set)");
+    if (!pl->hB2 && cudaMalloc(&pl->hB2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B (2nd set)");
+    if (!pl->hC2 && cudaMalloc(&pl->hC2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C (2nd set)");
+  }
+  if (async) {
+    for (cudaEvent_t* e : {&pl->set_free[0], &pl->set_free[1], &pl->compute_done})
+      if (!*e) MF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    if (!pl->cs1) MF_CUDA(cudaStreamCreateWithFlags(&pl->cs1, cudaStreamNonBlocking), "stream");
+  }
+  double* const setA = set ? pl->hA2 : pl->hA;
+  double* const setB = set ? pl->hB2 : pl->hB;
+  double* const setC = set ? pl->hC2 : pl->hC;
+  cudaStream_t const cs_main = async ? pl->cs1 : s;  // first compute stream
   if (!pl->h2d) MF_CUDA(cudaStreamCreateWithFlags(&pl->h2d, cudaStreamNonBlocking), "stream");
   if (!pl->d2h) MF_CUDA(cudaStreamCreateWithFlags(&pl->d2h, cudaStreamNonBlocking), "stream");
   if (!pl->s2) MF_CUDA(cudaStreamCreateWithFlags(&pl->s2, cudaStreamNonBlocking), "stream");
@@ -1240,21 +1299,28 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   cudaEvent_t* e_pa = e_b + nc;             // K4(A_i) done
   cudaEvent_t* e_pb = e_pa + ns;            // K4(B_j) done
   cudaEvent_t* e_c = e_pb + nc;             // region done
-  const double* dA = pl->hA;
-  const double* dB = pl->hB;
-  double* dC = pl->hC;
+  const double* dA = setA;
+  const double* dB = setB;
+  double* dC = setC;
   int region_no = 0;
 
-  MF_CUDA(cudaEventRecord(e_start, s), "event");
-  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
-    MF_CUDA(cudaStreamWaitEvent(st, e_start, 0), "wait");
+  if (!async) {
+    MF_CUDA(cudaEventRecord(e_start, s), "event");
+    for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2})
+      MF_CUDA(cudaStreamWaitEvent(st, e_start, 0), "wait");
+  } else {
+    // inputs may overwrite this set once its previous user's D2H is done;
+    // K4 rewrites the shared T/S workspace once the previous call's leaves ran
+    if (pl->set_busy[set]) MF_CUDA(cudaStreamWaitEvent(pl->h2d, pl->set_free[set], 0), "wait");
+    if (pl->compute_pending) MF_CUDA(cudaStreamWaitEvent(pl->mixs, pl->compute_done, 0), "wait");
+  }
   // h2d: A_0, B_0, A_1, B_1, ...
   for (int k = 0; k < std::max(ns, nc); ++k) {
     if (k < ns) {
       const auto sr = tile_piece(m, k, ns);
       for (int br = 0; br < P; ++br) {
         const int64_t row = br * m + sr.first;
-        MF_CUDA(cudaMemcpy2DAsync(pl->hA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
+        MF_CUDA(cudaMemcpy2DAsync(setA + row * n, n * 8, A + row * lda, lda * 8, n * 8,
                                   sr.second - sr.first, cudaMemcpyHostToDevice, pl->h2d), "H2D A slab");
       }
       MF_CUDA(cudaEventRecord(e_a[k], pl->h2d), "event");
@@ -1262,7 +1328,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     if (k < nc) {
       const auto sc = tile_piece(m, k, nc);
       for (int bc = 0; bc < P; ++bc)
-        MF_CUDA(cudaMemcpy2DAsync(pl->hB + bc * m + sc.first, n * 8, B + bc * m + sc.first, ldb * 8,
+        MF_CUDA(cudaMemcpy2DAsync(setB + bc * m + sc.first, n * 8, B + bc * m + sc.first, ldb * 8,
                                   (sc.second - sc.first) * 8, n, cudaMemcpyHostToDevice, pl->h2d),
                 "H2D B slab");
       MF_CUDA(cudaEventRecord(e_b[k], pl->h2d), "event");
@@ -1291,7 +1357,7 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
   }
   // regions in shells, alternating compute streams
   auto region = [&](int i, int j) -> mf_status {
-    cudaStream_t cs = (region_no & 1) ? pl->s2 : s;
+    cudaStream_t cs = (region_no & 1) ? pl->s2 : cs_main;
     MF_CUDA(cudaStreamWaitEvent(cs, e_pa[i], 0), "wait");
     MF_CUDA(cudaStreamWaitEvent(cs, e_pb[j], 0), "wait");
     const auto sr = tile_piece(m, i, ns);
@@ -1325,6 +1391,19 @@ mf_status mf_dgemm_host(mf_plan_t pl, double alpha, const double* A, int64_t lda
     if (k < nc)
       for (int i = 0; i <= std::min(k, ns - 1); ++i)
         if ((st = region(i, k)) != MF_OK) return st;
+  }
+  if (async) {
+    // compute done (both compute streams) -> the next call's K4 may start;
+    // last D2H done -> this set is free; the caller's stream ends after both
+    MF_CUDA(cudaEventRecord(e_s2, pl->s2), "event");
+    MF_CUDA(cudaStreamWaitEvent(pl->cs1, e_s2, 0), "wait");
+    MF_CUDA(cudaEventRecord(pl->compute_done, pl->cs1), "event");
+    pl->compute_pending = true;
+    MF_CUDA(cudaEventRecord(pl->set_free[set], pl->d2h), "event");
+    pl->set_busy[set] = true;
+    MF_CUDA(cudaStreamWaitEvent(s, pl->set_free[set], 0), "wait");
+    ++pl->async_calls;
+    return MF_OK;
   }
   MF_CUDA(cudaEventRecord(e_done, pl->d2h), "event");
   MF_CUDA(cudaEventRecord(e_s2, pl->s2), "event");

@@ -146,6 +146,16 @@ struct Plan {
   int n_jobs = 0;
   // host-buffer path (mf_dgemm_host): device copies of A, B, C
   double *hA = nullptr, *hB = nullptr, *hC = nullptr;
+  // mf_dgemm_host_async: a second device set (calls alternate between the two),
+  // the event that frees each set (its last D2H), the previous call's compute
+  // completion, and the plan-owned first compute stream of async calls
+  double *hA2 = nullptr, *hB2 = nullptr, *hC2 = nullptr;
+  cudaEvent_t set_free[2] = {nullptr, nullptr};
+  bool set_busy[2] = {false, false};
+  cudaEvent_t compute_done = nullptr;
+  bool compute_pending = false;
+  cudaStream_t cs1 = nullptr;
+  int64_t async_calls = 0;
   // NCCL
   void* nccl_comm = nullptr;
   cudaEvent_t done = nullptr;

@@ -822,3 +822,33 @@ def test_three_level_sharding_n8(regions):
             total += p.dgemm(Ad, Bd)
     A, B, C = host(Ad), host(Bd), host(total)
     assert oracle.freivalds_int(A, B, C, trials=2) == 0
+
+
+# ------------------------------------------------ asynchronous host-buffer stream
+
+@pytest.mark.parametrize("name,levels,n,kw", [(SW, 2, 2048, {}), (SW, 1, 1000, {}), (None, 0, 1024, {}),
+                                              (SW, 2, 1024, {"level_by_level": True})])
+def test_host_async_stream_matches_sync(name, levels, n, kw):
+    """mf_dgemm_host_async: a stream of 5 products with different pinned inputs,
+    enqueued back to back (two device sets, call k+1's copies under call k's
+    compute), then mf_host_sync: every C bitwise the synchronous call's.  A
+    synchronous call after async ones waits for them; plans without the region
+    pipeline (level by level) run synchronously."""
+    t = triples.get(name) if name else None
+    with mf.Plan(t, levels, n, **kw) as p:
+        ins, outs, refs = [], [], []
+        for k in range(5):
+            A, B = mf_inputs.pair("uniform", n, 70 + k)
+            Ah = torch.from_numpy(A).pin_memory(); Bh = torch.from_numpy(B).pin_memory()
+            Ch = torch.full((n, n), float("nan"), dtype=torch.float64).pin_memory()
+            ins.append((Ah, Bh)); outs.append(Ch)
+            refs.append(p.dgemm_host(A, B, alpha=0.5))
+        for (Ah, Bh), Ch in zip(ins, outs):
+            p.dgemm_host_async_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n, alpha=0.5)
+        p.host_sync()
+        for Ch, ref in zip(outs, refs):
+            assert (Ch.numpy() == ref).all()
+        Ai, Bi = mf_inputs.pair("int1024", n, 80)
+        p.dgemm_host_async_ptr(ins[0][0].data_ptr(), n, ins[0][1].data_ptr(), n, outs[0].data_ptr(), n)
+        assert (p.dgemm_host(Ai, Bi) == exact(Ai, Bi)).all()  # drains the async call first
+        assert (outs[0].numpy() == 2.0 * refs[0]).all()
