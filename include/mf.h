@@ -253,6 +253,20 @@ mf_status mf_nccl_unique_id(void* id_out /* 128 bytes */);
 mf_status mf_nccl_comm_create(void** comm_out, const void* id, int32_t rank, int32_t nranks);
 mf_status mf_nccl_comm_destroy(void* comm);
 
+/* Diagnostic: generate the fused-addition kernel mf_plan would build at run
+ * time (NVRTC) for one coefficient table -- coef is nout x nin row-major
+ * (coef[o*nin + k] = coefficient of input k in output o, 0 = absent; Eq.
+ * "strassen") -- with inputs / outputs addressed as the
+ * blocks of a P x P partition (in_P / out_P > 0) or as [slots][m][m] (0), and
+ * compile it for `arch` (e.g. "sm_100a").  Needs no GPU.  *vw_out = positions
+ * per thread chosen (0 = table too large for a generated kernel);
+ * *cubin_bytes = size of the compiled code.  MF_ERR_UNSUPPORTED when NVRTC is
+ * missing, the table does not fit, or compilation fails (message in
+ * mf_last_error). */
+mf_status mf_jit_compile_check(const double* coef, int32_t nout, int32_t nin, int32_t in_P,
+                               int32_t out_P, const char* arch, int32_t* vw_out,
+                               int64_t* cubin_bytes);
+
 /* Library version, e.g. "mf 0.1.0 sm_100a". */
 const char* mf_version(void);
 

@@ -40,7 +40,7 @@ OUT_ROOT, OUT_ALL, OUT_ROWSLAB = 0, 1, 2
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
            "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
-           "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync")
+           "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync", "mf_jit_compile_check")
 
 
 class mf_options(ctypes.Structure):
@@ -76,6 +76,8 @@ _lib.mf_profile_read.argtypes = [_P, _P, ctypes.POINTER(_I32), _I32]
 _lib.mf_nccl_unique_id.argtypes = [_P]
 _lib.mf_nccl_comm_create.argtypes = [ctypes.POINTER(_P), _P, _I32, _I32]
 _lib.mf_nccl_comm_destroy.argtypes = [_P]
+_lib.mf_jit_compile_check.argtypes = [_P, _I32, _I32, _I32, _I32, ctypes.c_char_p,
+                                      ctypes.POINTER(_I32), ctypes.POINTER(_I64)]
 for _f in EXPORTS:
     if _f not in ("mf_last_error", "mf_version"):
         getattr(_lib, _f).restype = ctypes.c_int
@@ -94,6 +96,17 @@ def _check(status: int):
 
 def version() -> str:
     return _lib.mf_version().decode()
+
+
+def jit_compile_check(coef, in_P: int, out_P: int, arch: str = "sm_100a"):
+    """mf_jit_compile_check: generate + compile (no GPU) the fused-addition
+    kernel of a coefficient table coef[nout][nin]; returns (vw, cubin_bytes)."""
+    import numpy as np
+    c = np.ascontiguousarray(coef, dtype=np.float64)
+    vw, nb = _I32(0), _I64(0)
+    _check(_lib.mf_jit_compile_check(c.ctypes.data, c.shape[0], c.shape[1], in_P, out_P,
+                                     arch.encode(), ctypes.byref(vw), ctypes.byref(nb)))
+    return vw.value, nb.value
 
 
 def _mat(X, n, name, rows=None):

@@ -212,8 +212,45 @@ void kron(int po, int64_t Ro, const std::vector<double>& Uo, const std::vector<d
     }
 }
 
+// Greedy output grouping for the grouped mix kernel: each group is seeded with
+// the first unassigned output and grown with the unassigned output sharing the
+// most inputs with the group (lowest index on ties), so a warp's loads serve as
+// many of its outputs as possible.  ngroup = ceil(nout / gsize), sizes differ
+// by at most one.
+static std::vector<std::vector<int>> group_outputs(const MixTable& t, int gsize) {
+  const int ng = (t.nout + gsize - 1) / gsize;
+  std::vector<std::vector<int>> groups;
+  std::vector<char> used(t.nout, 0);
+  auto uses = [&](int o, int k) { return t.coef[(size_t)o * t.nin + k] != 0.0; };
+  for (int g = 0; g < ng; ++g) {
+    const int size = t.nout / ng + (g < t.nout % ng ? 1 : 0);
+    std::vector<int> grp;
+    std::vector<char> in_union(t.nin, 0);
+    for (int o = 0; o < t.nout && grp.empty(); ++o)
+      if (!used[o]) { grp.push_back(o); used[o] = 1; }
+    if (grp.empty()) break;
+    for (int k = 0; k < t.nin; ++k) in_union[k] = uses(grp[0], k);
+    while ((int)grp.size() < size) {
+      int best = -1, best_shared = -1;
+      for (int o = 0; o < t.nout; ++o) {
+        if (used[o]) continue;
+        int shared = 0;
+        for (int k = 0; k < t.nin; ++k) shared += in_union[k] && uses(o, k);
+        if (shared > best_shared) { best = o; best_shared = shared; }
+      }
+      if (best < 0) break;
+      grp.push_back(best);
+      used[best] = 1;
+      for (int k = 0; k < t.nin; ++k) in_union[k] = in_union[k] || uses(best, k);
+    }
+    groups.push_back(grp);
+  }
+  return groups;
+}
+
 // Device table: MixRow[nout] then MixTerm[...] -- each output's nonzero
-// terms in ascending input order (the oracle's combination order).
+// terms in ascending input order (the oracle's combination order) -- then the
+// grouped form (MixGroup[ngroup], entries) when it fits in shared memory.
 mf_status upload_table(MixTable& t) {
   std::vector<MixRow> rows;
   std::vector<MixTerm> terms;
@@ -238,13 +275,59 @@ mf_status upload_table(MixTable& t) {
   const size_t bytes = sizeof(MixRow) * rows.size() + sizeof(MixTerm) * terms.size();
   if (bytes == 0) return MF_OK;
   if (bytes > 200 * 1024) return fail(MF_ERR_UNSUPPORTED, "mix table of %zu bytes exceeds shared memory", bytes);
-  MF_CUDA(cudaMalloc(&t.d_table, bytes), "cudaMalloc(coefficient table)");
+  // grouped form: one group per warp of a 256-thread CTA.  Measured against
+  // the term-list kernel it wins up to 4 outputs per warp (LD K4, every K6)
+  // and loses beyond (SW^2 K4: 5 per warp, 4.2 vs 3.4 ms; profiles/mix_r01.json)
+  std::vector<uint8_t> gtab;
+  t.gsize = t.ngroup = 0;
+  const int gsize = std::max(1, (t.nout + 7) / 8);
+  if (!getenv("MF_MIX_UNGROUPED") && gsize <= 4) {
+    const auto groups = group_outputs(t, gsize);
+    std::vector<MixGroup> hdr;
+    std::vector<uint8_t> ent;
+    const size_t stride = 8 + 8 * (size_t)gsize;
+    for (const auto& grp : groups) {
+      MixGroup h{};
+      h.first = (int32_t)(ent.size() / stride);
+      for (int j = 0; j < MIX_GMAX; ++j) h.target[j] = j < (int)grp.size() ? t.out_map[grp[j]] : -1;
+      for (int k = 0; k < t.nin; ++k) {
+        bool any = false;
+        for (int o : grp) any = any || t.coef[(size_t)o * t.nin + k] != 0.0;
+        if (!any) continue;
+        std::vector<uint8_t> e(stride, 0);
+        const int32_t src = k;
+        memcpy(e.data(), &src, 4);
+        for (int j = 0; j < (int)grp.size(); ++j) {
+          const double v = t.coef[(size_t)grp[j] * t.nin + k];
+          memcpy(e.data() + 8 + 8 * j, &v, 8);
+        }
+        ent.insert(ent.end(), e.begin(), e.end());
+      }
+      h.count = (int32_t)(ent.size() / stride) - h.first;
+      hdr.push_back(h);
+    }
+    const size_t gb = sizeof(MixGroup) * hdr.size() + ent.size();
+    if (gb <= 96 * 1024) {
+      gtab.resize(gb);
+      memcpy(gtab.data(), hdr.data(), sizeof(MixGroup) * hdr.size());
+      memcpy(gtab.data() + sizeof(MixGroup) * hdr.size(), ent.data(), ent.size());
+      t.gsize = gsize;
+      t.ngroup = (int)hdr.size();
+    }
+  }
+  t.goff = (bytes + 15) / 16 * 16;
+  t.gbytes = gtab.size();
+  MF_CUDA(cudaMalloc(&t.d_table, t.goff + t.gbytes), "cudaMalloc(coefficient table)");
   MF_CUDA(cudaMemcpy(t.d_table, rows.data(), sizeof(MixRow) * rows.size(), cudaMemcpyHostToDevice),
           "upload table");
   if (!terms.empty())
     MF_CUDA(cudaMemcpy(static_cast<uint8_t*>(t.d_table) + sizeof(MixRow) * rows.size(), terms.data(),
                        sizeof(MixTerm) * terms.size(), cudaMemcpyHostToDevice),
             "upload table");
+  if (!gtab.empty())
+    MF_CUDA(cudaMemcpy(static_cast<uint8_t*>(t.d_table) + t.goff, gtab.data(), gtab.size(),
+                       cudaMemcpyHostToDevice),
+            "upload grouped table");
   return MF_OK;
 }
 
@@ -269,9 +352,12 @@ void free_plan(Plan* pl) {
   for (cudaEvent_t e : pl->comm_events) cudaEventDestroy(e);
   for (cudaEvent_t e : {pl->set_free[0], pl->set_free[1], pl->compute_done})
     if (e) cudaEventDestroy(e);
-  for (auto& b : pl->batches)
+  for (auto& b : pl->batches) {
     for (void* p : {b.mixA.d_table, b.mixB.d_table, b.mixC.d_table})
       if (p) cudaFree(p);
+    for (MixTable* t : {&b.mixA, &b.mixB, &b.mixC}) jit_free(*t);
+  }
+  for (MixTable* t : {&pl->mixA, &pl->mixB, &pl->mixC, &pl->mixA2, &pl->mixC2}) jit_free(*t);
   for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm, pl->cs1})
     if (st) cudaStreamDestroy(st);
 }
@@ -707,6 +793,19 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       free_plan(pl.get());
       return st;
     }
+    // triples without compiled-in K4/K6, and the local tables of batches:
+    // generate and compile their kernels now (mf_jit.cpp)
+    std::vector<JitJob> jj;
+    if (pl->fixed_id == 0 && levels > 0) {
+      for (MixTable* t : {&pl->mixA, &pl->mixA2, &pl->mixB}) jj.push_back({t, pl->P, 0});
+      for (MixTable* t : {&pl->mixC, &pl->mixC2}) jj.push_back({t, 0, pl->P});
+    }
+    for (auto& b : pl->batches) {
+      jj.push_back({&b.mixA, pl->P, 0});
+      jj.push_back({&b.mixB, pl->P, 0});
+      jj.push_back({&b.mixC, 0, pl->P});
+    }
+    jit_build_all(jj);
   }
   std::vector<LeafJob> jobs;
   std::vector<int32_t> job_q = pl->my_prods;
@@ -1410,6 +1509,31 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
   MF_CUDA(cudaStreamWaitEvent(s, e_s2, 0), "wait");    // the call's stream ends after all work
   MF_CUDA(cudaStreamWaitEvent(s, e_done, 0), "wait");
   MF_CUDA(cudaEventSynchronize(e_done), "cudaEventSynchronize");
+  return MF_OK;
+}
+
+// Diagnostic entry (include/mf.h): generate and compile the kernel of one
+// coefficient table for an architecture, without a GPU -- the CPU tests use it
+// to check the generator's output compiles.
+mf_status mf_jit_compile_check(const double* coef, int32_t nout, int32_t nin,
+                               int32_t in_P, int32_t out_P, const char* arch,
+                               int32_t* vw_out, int64_t* cubin_bytes) {
+  g_err.clear();
+  if (!coef || nout <= 0 || nin <= 0 || in_P < 0 || out_P < 0 || !arch)
+    return fail(MF_ERR_INVALID_ARG, "bad argument");
+  MixTable t;
+  t.nin = nin;
+  t.nout = nout;
+  t.coef.assign(coef, coef + (size_t)nout * nin);
+  for (int o = 0; o < nout; ++o) t.out_map.push_back(o);
+  const JitShape sh = jit_shape(t);
+  if (vw_out) *vw_out = sh.vw;
+  if (sh.vw == 0) return fail(MF_ERR_UNSUPPORTED, "table too large for a generated kernel");
+  std::vector<char> cubin;
+  std::string log;
+  if (!jit_compile(jit_source(t, in_P, out_P, sh), arch, cubin, log))
+    return fail(MF_ERR_UNSUPPORTED, "NVRTC: %.400s", log.c_str());
+  if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
   return MF_OK;
 }
 

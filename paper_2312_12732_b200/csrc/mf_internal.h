@@ -68,13 +68,49 @@ struct MixTerm {
   double coef;   // used when kind == MIX_GEN
 };
 
+// Grouped form (the kernel used when it fits): outputs in groups of `gsize`
+// (<= MIX_GMAX) that share inputs; a group lists the union of its outputs'
+// inputs in ascending order, each entry carrying one coefficient per output
+// (0 = absent), so a warp loads every input of its group once and updates all
+// of the group's accumulators from registers.  Entry e of the device table is
+// {int32 src, int32 pad, double coef[gsize]} (8 + 8*gsize bytes).
+constexpr int MIX_GMAX = 4;
+struct MixGroup {
+  int32_t first, count;           // entries [first, first+count)
+  int32_t target[MIX_GMAX];       // output block / slot per member, -1 = none
+};
+
 struct MixTable {
   int nin = 0, nout = 0;
   std::vector<double> coef;      // nout x nin
   std::vector<int32_t> out_map;  // output o -> slot / C block it writes
   int nrow = 0, nterm = 0;       // device table sizes
-  void* d_table = nullptr;       // device MixRow + MixTerm table (owned by the plan)
+  void* d_table = nullptr;       // device MixRow + MixTerm table (owned by the plan),
+                                 // then the grouped table at byte offset goff
+  int gsize = 0, ngroup = 0;     // grouped form (gsize 0 = not built)
+  size_t goff = 0, gbytes = 0;
+  // kernel generated for this table at plan time (mf_jit.cpp; CUmodule /
+  // CUfunction, owned by the plan), 0 = none
+  void* jit_mod = nullptr;
+  void* jit_fn = nullptr;
+  int jit_vw = 0;
 };
+
+// mf_jit.cpp: K4/K6 generated per table (NVRTC) -- register shape, source,
+// compile, load, launch
+struct JitShape {
+  int vw = 0;               // positions per thread (0 = does not fit)
+  bool input_major = false; // accumulators held (true) or inputs held
+};
+JitShape jit_shape(const MixTable& t);
+std::string jit_source(const MixTable& t, int in_P, int out_P, const JitShape& sh);
+bool jit_compile(const std::string& src, const char* arch, std::vector<char>& cubin, std::string& log);
+struct JitJob {
+  MixTable* t;
+  int in_P, out_P;  // partition factor of a block view, 0 = slot view
+};
+int jit_build_all(const std::vector<JitJob>& jobs);
+void jit_free(MixTable& t);
 
 struct Plan {
   int device = 0;
@@ -189,6 +225,11 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
 cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, const double* Pw,
                            double* C, int64_t ldc, cudaStream_t s, Rows rows = Rows(),
                            bool accumulate = false);
+
+// mf_jit.cpp: launch a table's generated kernel; cudaErrorNotSupported when
+// it has none or cannot serve these views (callers then use mf_mix.cu's)
+cudaError_t jit_launch(const MixTable& t, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                       int64_t m, double alpha, Rows rows, int accumulate, cudaStream_t s);
 
 struct LeafArgs {
   // operand views: matrices (4-D block view, SRC_INPUT) and workspaces (3-D)

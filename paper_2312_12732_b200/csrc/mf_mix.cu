@@ -158,6 +158,90 @@ __global__ void __launch_bounds__(256) mix_kernel(View in, View out, int64_t m,
   }
 }
 
+// Grouped K4/K6 (default when the table fits): warp w owns output groups
+// w, w+8, ...; for each input in its group's union (ascending), it loads the
+// input once and adds it into every member that uses it (warp-uniform
+// coefficients from shared memory, zero = absent).  Each output still sums
+// its own terms in ascending input order -- the oracle's order, bit-exact --
+// but a CTA now reads each input about once per group instead of once per
+// term, which is what bounded the term-list kernel (on-chip traffic, not HBM).
+template <int VW, int G>
+__global__ void __launch_bounds__(256) mix_group_kernel(View in, View out, int64_t m,
+                                                        const void* __restrict__ table,
+                                                        int ngroup, int tbytes, double alpha,
+                                                        int64_t r0, int64_t r1, int64_t c0,
+                                                        int64_t c1, int accumulate) {
+  extern __shared__ __align__(16) uint8_t s_raw[];
+  for (int i = threadIdx.x; i < tbytes / 8; i += blockDim.x)
+    reinterpret_cast<uint64_t*>(s_raw)[i] = reinterpret_cast<const uint64_t*>(table)[i];
+  __syncthreads();
+  const MixGroup* groups = reinterpret_cast<const MixGroup*>(s_raw);
+  const uint8_t* ents = reinterpret_cast<const uint8_t*>(groups + ngroup);
+  constexpr int STRIDE = 8 + 8 * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int SEG = 32 * VW;
+  const int64_t segs_per_row = (c1 - c0 + SEG - 1) / SEG;
+  const int64_t total = (r1 - r0) * segs_per_row;
+  for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
+    const int64_t rr = seg / segs_per_row;
+    const int64_t r = r0 + rr;
+    const int64_t c = c0 + (seg - rr * segs_per_row) * SEG + lane * VW;
+    if (c >= c1) continue;
+    for (int g = warp; g < ngroup; g += 8) {
+      const int first = groups[g].first, count = groups[g].count;
+      Vec<VW> acc[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+#pragma unroll
+        for (int e = 0; e < VW; ++e) acc[j].v[e] = -0.0;
+      auto apply = [&](const uint8_t* en, const Vec<VW>& x) {
+        const double* cf = reinterpret_cast<const double*>(en + 8);
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          const double cj = cf[j];
+          if (cj == 1.0) {
+            add_term<VW>(acc[j], x, MIX_POS, cj);
+          } else if (cj == -1.0) {
+            add_term<VW>(acc[j], x, MIX_NEG, cj);
+          } else if (cj != 0.0) {
+            add_term<VW>(acc[j], x, MIX_GEN, cj);
+          }
+        }
+      };
+      int e = 0;
+      for (; e + 1 < count; e += 2) {  // two loads in flight per step
+        const uint8_t* e0 = ents + (size_t)(first + e) * STRIDE;
+        const uint8_t* e1 = e0 + STRIDE;
+        const Vec<VW> x0 = load_vec<VW>(in.at(*reinterpret_cast<const int32_t*>(e0), m, r, c));
+        const Vec<VW> x1 = load_vec<VW>(in.at(*reinterpret_cast<const int32_t*>(e1), m, r, c));
+        apply(e0, x0);
+        apply(e1, x1);
+      }
+      if (e < count) {
+        const uint8_t* e0 = ents + (size_t)(first + e) * STRIDE;
+        apply(e0, load_vec<VW>(in.at(*reinterpret_cast<const int32_t*>(e0), m, r, c)));
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int target = groups[g].target[j];
+        if (target < 0) continue;
+        Vec<VW> v = acc[j];
+        if (alpha != 1.0) {
+#pragma unroll
+          for (int q = 0; q < VW; ++q) v.v[q] = __dmul_rn(alpha, v.v[q]);
+        }
+        double* dst = out.at(target, m, r, c);
+        if (accumulate) {
+          const Vec<VW> old = load_vec<VW>(dst);
+#pragma unroll
+          for (int q = 0; q < VW; ++q) v.v[q] = __dadd_rn(old.v[q], v.v[q]);
+        }
+        store_vec<VW>(dst, v);
+      }
+    }
+  }
+}
+
 bool aligned(const void* p, int bytes) { return ((uintptr_t)p % bytes) == 0; }
 
 // Grid: `work` items of `per_block` each, capped at 8 CTAs (of 256 threads) per SM.
@@ -201,11 +285,44 @@ static int pick_vw(int64_t m, std::initializer_list<std::pair<const void*, int64
   return 1;
 }
 
+template <int VW, int G>
+static cudaError_t group_launch(const MixTable& t, View in, View out, int64_t m, double alpha,
+                               cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                               int accumulate) {
+  const int smem = (int)t.gbytes;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(mix_group_kernel<VW, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  mix_group_kernel<VW, G><<<grid_for((r1 - r0) * ((c1 - c0 + 32 * VW - 1) / (32 * VW)), 1), 256,
+                            smem, s>>>(in, out, m, static_cast<const uint8_t*>(t.d_table) + t.goff,
+                                       t.ngroup, smem, alpha, r0, r1, c0, c1, accumulate);
+  return cudaGetLastError();
+}
+
+template <int VW>
+static cudaError_t group_dispatch(const MixTable& t, View in, View out, int64_t m, double alpha,
+                                  cudaStream_t s, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                                  int accumulate) {
+  switch (t.gsize) {
+    case 1: return group_launch<VW, 1>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+    case 2: return group_launch<VW, 2>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+    case 3: return group_launch<VW, 3>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+    default: return group_launch<VW, 4>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+  }
+}
+
 static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, int64_t m,
                                 double alpha, cudaStream_t s, Rows rows, int accumulate = 0) {
   if (t.nrow == 0) return cudaSuccess;
   const int64_t r0 = rows.r0, r1 = rows.end(m), c0 = rows.c0, c1 = rows.cend(m);
   if (r1 <= r0 || c1 <= c0) return cudaSuccess;
+  if (t.gsize > 0) {
+    if (vw == 4) return group_dispatch<4>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+    if (vw == 2) return group_dispatch<2>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+    return group_dispatch<1>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
+  }
   if (vw == 4) return mix_launch<4>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
   if (vw == 2) return mix_launch<2>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
   return mix_launch<1>(t, in, out, m, alpha, s, r0, r1, c0, c1, accumulate);
@@ -224,6 +341,8 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
     if (fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
       return launch_premix_fixed(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
   }
+  const cudaError_t j = jit_launch(t, X, ldx, out, pl.m, pl.m, 1.0, rows, 0, s);
+  if (j != cudaErrorNotSupported) return j;
   const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
   return mix_dispatch(vw, t, View{const_cast<double*>(X), ldx, pl.P}, View{out, pl.m, 0}, pl.m,
                       1.0, s, rows);
@@ -238,6 +357,8 @@ cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, cons
     if (fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
       return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
   }
+  const cudaError_t j = jit_launch(t, Pw, pl.m, C, ldc, pl.m, alpha, rows, accumulate ? 1 : 0, s);
+  if (j != cudaErrorNotSupported) return j;
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
   return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
                       pl.m, alpha, s, rows, accumulate ? 1 : 0);

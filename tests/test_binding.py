@@ -201,3 +201,34 @@ def test_output_mode_and_leaf_validation():
     st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, leaf=mf.LEAF_CUBLAS, fuse_postadd=1,
                            host_only=1)
     assert st == mf.MF_ERR_UNSUPPORTED
+
+
+def test_jit_generator_compiles_without_gpu():
+    """mf_jit_compile_check (include/mf.h): the plan-time K4/K6 generator emits
+    CUDA that NVRTC compiles for sm_100a here, on the GPU-less box -- the
+    output-major shape for a pre-addition (16 inputs held, 256-bit vectors) and
+    the input-major shape for a post-addition (16 accumulators, 128-bit);
+    tables too large for registers are refused, not miscompiled."""
+    import numpy as np
+    from paper_2312_12732_b200 import triples
+    sw = triples.get("strassen-winograd")
+    f = triples.kron(sw, sw)
+    U = np.array(f.U, dtype=float).reshape(16, 49)
+    W = np.array(f.W, dtype=float).reshape(16, 49)
+    mat = [q for q in range(49) if np.count_nonzero(U[:, q]) != 1]
+    try:
+        vw, nb = mf.jit_compile_check(U[:, mat].T, 4, 0)
+    except mf.MfError as e:
+        if "NVRTC not available" in str(e):
+            pytest.skip("no NVRTC in this image")
+        raise
+    assert vw == 4 and nb > 0
+    vw, nb = mf.jit_compile_check(W, 0, 4)
+    assert vw == 2 and nb > 0
+    # a non-unit coefficient (hex literal, exact) and alpha paths compile too
+    vw, _ = mf.jit_compile_check(np.array([[0.5, -3.0, 1.0]]), 0, 0)
+    assert vw == 4
+    big = np.ones((80, 80))
+    with pytest.raises(mf.MfError) as e:
+        mf.jit_compile_check(big, 0, 0)
+    assert e.value.status == mf.MF_ERR_UNSUPPORTED

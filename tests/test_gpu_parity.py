@@ -109,14 +109,20 @@ def _kron_factored(name, levels, path):
     return path == "fixed" and deep
 
 
-MIX_PATHS = ["fixed", "generic"]  # compile-time specialised K4/K6 vs table-driven kernels
+# compile-time specialised K4/K6 vs the plan-time generated kernels (NVRTC,
+# the default for triples without compiled-in kernels) vs the table-driven
+# kernels: grouped and the per-output term-list kernel (MF_MIX_UNGROUPED)
+MIX_PATHS = ["fixed", "jit", "generic", "generic-terms"]
 
 
 def _mix_path(monkeypatch, path):
-    if path == "generic":
-        monkeypatch.setenv("MF_MIX_GENERIC", "1")
-    else:
-        monkeypatch.delenv("MF_MIX_GENERIC", raising=False)
+    for var, on in (("MF_MIX_GENERIC", path != "fixed"),
+                    ("MF_MIX_NOJIT", path.startswith("generic")),
+                    ("MF_MIX_UNGROUPED", path == "generic-terms")):
+        if on:
+            monkeypatch.setenv(var, "1")
+        else:
+            monkeypatch.delenv(var, raising=False)
 
 
 @pytest.mark.parametrize("path", MIX_PATHS)
@@ -454,12 +460,15 @@ def run_plan(p, A, B):
     return host(p.dgemm(dev(A), dev(B)))
 
 
+@pytest.mark.parametrize("path", ["jit", "generic"])
 @pytest.mark.parametrize("name,levels,n,g", [(SW, 2, 512, 5), ("laderman", 1, 288, 2), (SW, 3, 256, 3),
                                              (SW, 1, 400, 1)])
-def test_bounded_workspace_batches(name, levels, n, g):
+def test_bounded_workspace_batches(name, levels, n, g, path, monkeypatch):
     """NEXT-3 bounded workspace: products run in batches
     of g whose T/S/P fit max_workspace; exact on integers, within the bound on
-    random inputs, workspace within the cap; too small a cap is reported."""
+    random inputs, workspace within the cap; too small a cap is reported.
+    Batches run generated K4/K6 (jit) or the table-driven kernels (generic)."""
+    _mix_path(monkeypatch, path)
     t = triples.get(name)
     m = n // t.p ** levels
     cap = 3 * g * m * m * 8
@@ -477,6 +486,26 @@ def test_bounded_workspace_batches(name, levels, n, g):
         C2 = host(p.dgemm(dev(A), dev(B), alpha=0.5))
     with mf.Plan(t, levels, n) as p:
         assert (C2 == host(p.dgemm(dev(A), dev(B), alpha=0.5))).all()
+
+
+@pytest.mark.parametrize("name,levels,n,cap_blocks", [(SW, 2, 512, 15), ("laderman", 2, 243, 6),
+                                                      (SW, 1, 200, None), ("laderman", 1, 120, None)])
+def test_jit_mix_bitwise_table_kernels(name, levels, n, cap_blocks, monkeypatch):
+    """The plan-time generated K4/K6 (mf_jit.cpp) and the table-driven kernels
+    sum every output in the same (the oracle's) order: bitwise equal results on
+    random inputs, whole plans and bounded-workspace batches (K6 accumulating
+    into C), ragged leaves (m = 100, 60: 64-bit vectors) included."""
+    t = triples.get(name)
+    m = n // t.p ** levels
+    kw = {"max_workspace": 3 * cap_blocks * m * m * 8} if cap_blocks else {}
+    A, B = mf_inputs.pair("uniform", n, 31)
+    out = {}
+    for path in ("jit", "generic"):
+        _mix_path(monkeypatch, path)
+        with mf.Plan(t, levels, n, **kw) as p:
+            out[path] = host(p.dgemm(dev(A), dev(B), alpha=1.5))
+    assert (out["jit"] == out["generic"]).all()
+    assert scaled(out["jit"], 1.5 * oracle.classical(A, B), A, B) <= 1e-13 * levels
 
 
 def test_host_buffer_entry_point():
