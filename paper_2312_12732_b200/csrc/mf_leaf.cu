@@ -17,7 +17,12 @@
 //    neighbouring block); a materialised operand is a slot of the T/S
 //    workspace (3-D map {col, row, slot}).
 //  * CTA tile 128 x BNT (BNT = 128, or 64 for badly filled last waves), k 32
-//    per ring stage (KSUB = 2 sub-blocks of 16; 3 stages in 192 KB).  Each
+//    per ring stage (KSUB = 2 sub-blocks of 16; 3 stages in 192 KB), or k 48
+//    (KSUB = 3, 2 stages) where m is a multiple of 48 or >= 8192.  A last
+//    stage past the block edge multiplies only its sub-blocks that hold data;
+//    that per-group guard also splits the DMMA stream into blocks ptxas
+//    schedules without the DEPBAR scoreboard waits it used to insert (leaf
+//    185.65 -> 183.92 ms at n=16384 SW^2, profiles/leaf_ksub_r01.json).  Each
 //    MMA warp owns 64 x BNT/4 of C: 64 fp64 accumulators per thread at
 //    BNT = 128.  Fragments are fetched with 128-bit LDS, which shared memory
 //    serves per quarter-warp (8 lanes).
@@ -284,7 +289,14 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     mbar_wait(full0, 0);
     load_frags(s_base, s_base + A_BYTES, 0, fa0, fb0);
   }
+  // fragment groups of the last stage that hold data: when m is not a
+  // multiple of the stage depth, the zero-filled k sub-blocks are not
+  // multiplied (a sub-block's two groups interleave its 16 k through the
+  // k-permutation, so the unit is the sub-block)
+  const int last_groups = 2 * (int)min((int64_t)KSUB,
+                                       (prm.m - (int64_t)(kb0 + nk - 1) * KS + BK - 1) / BK);
   for (int kb = 0; kb < nk; ++kb) {  // kb: stage index within this block's k-range
+    const int ngv = kb == nk - 1 ? last_groups : 2 * KSUB;
     if (warp == 0) {
       const int kn = kb + STAGES - 1;  // refill the slot consumed at kb - 1
       if (kn < nk) {
@@ -297,7 +309,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
     for (int gg = 0; gg < 2 * KSUB; gg += 2) {
       load_frags(sA, sB, gg + 1, fa1, fb1);  // group gg+1 of this stage
-      mma_group(fa0, fb0);                   // group gg
+      if (gg < ngv) mma_group(fa0, fb0);     // group gg
       if (gg + 2 < 2 * KSUB) {
         load_frags(sA, sB, gg + 2, fa0, fb0);
       } else {                               // last group: release, prefetch next stage
@@ -310,7 +322,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           load_frags(nA, nA + A_BYTES, 0, fa0, fb0);
         }
       }
-      mma_group(fa1, fb1);                   // group gg+1
+      if (gg + 1 < ngv) mma_group(fa1, fb1); // group gg+1
     }
   }
 
@@ -606,8 +618,12 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (cfg.split > 1 && (!a.split_ws || a.split_ws_elems < cfg.ws_elems || a.split_cnt_len < cfg.n_tail))
       cfg.split = 1;
     const int bn = cfg.bn;
-    int ksub = 2;  // k sub-blocks of 16 per pipeline stage
-    if (const char* e = getenv("MF_LEAF_KSUB")) ksub = atoi(e) == 1 ? 1 : 2;
+    // k sub-blocks of 16 per pipeline stage: 2 (k = 32, 3-stage ring), or 3
+    // (k = 48, 2 stages) where m is a multiple of 48 or large -- measured
+    // +0.2% there, -0.3% at m = 4096 (profiles/leaf_ksub_r01.json)
+    int ksub = (a.m % 48 == 0 || a.m >= 8192) && bn == 128 ? 3 : 2;
+    if (const char* e = getenv("MF_LEAF_KSUB")) ksub = std::min(3, std::max(1, atoi(e)));
+    if (ksub == 3 && bn != 128) ksub = 2;
     const bool fuse = a.post != nullptr;
     if (fuse) ksub = 2;  // the fused tile is staged in the KSUB=2 ring
     CUtensorMap mA, mT, mB, mS;
@@ -642,8 +658,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)
-    static std::atomic<uint64_t> attr_set[6];
-    const int inst = fuse ? (bn == 64 ? 5 : 4) : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0);
+    static std::atomic<uint64_t> attr_set[7];
+    const int inst = fuse ? (bn == 64 ? 5 : 4)
+                          : (ksub == 3 ? 6 : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0));
     const uint64_t dev_bit = 1ull << (dev & 63);
     auto launch = [&](auto kern, int smem) -> cudaError_t {
       if (!(attr_set[inst].load() & dev_bit)) {
@@ -661,6 +678,7 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
       case 2: e = launch(leaf_dmma_kernel<64, 1, false>, smem_bytes<64, 1>()); break;
       case 3: e = launch(leaf_dmma_kernel<64, 2, false>, smem_bytes<64, 2>()); break;
       case 4: e = launch(leaf_dmma_kernel<128, 2, true>, smem_bytes<128, 2>()); break;
+      case 6: e = launch(leaf_dmma_kernel<128, 3, false>, smem_bytes<128, 3>()); break;
       default: e = launch(leaf_dmma_kernel<64, 2, true>, smem_bytes<64, 2>()); break;
     }
     if (e != cudaSuccess) return e;
