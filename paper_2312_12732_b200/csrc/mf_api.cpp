@@ -1463,6 +1463,7 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
     const auto sc = tile_piece(m, j, nc);
     Rows rg;
     rg.r0 = sr.first; rg.r1 = sr.second; rg.c0 = sc.first; rg.c1 = sc.second;
+    rg.overlapped = true;  // regions alternate over two compute streams
     if (pl->levels == 0) {
       if ((st = run_leaf(*pl, dA, n, dB, n, nullptr, nullptr, dC, n, 0, alpha, cs, rg)) != MF_OK) return st;
     } else {

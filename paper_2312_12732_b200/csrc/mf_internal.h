@@ -215,6 +215,10 @@ struct Plan {
 struct Rows {
   int64_t r0 = 0, r1 = -1;  // r1 < 0 => m
   int64_t c0 = 0, c1 = -1;  // c1 < 0 => m
+  // the launch shares the GPU with concurrent launches on another stream (the
+  // host pipeline's alternating regions): the leaf keeps 128-wide tiles, the
+  // other stream fills its partial last wave
+  bool overlapped = false;
   int64_t end(int64_t m) const { return r1 < 0 ? m : r1; }
   int64_t cend(int64_t m) const { return c1 < 0 ? m : c1; }
 };
