@@ -53,6 +53,23 @@
 namespace mf {
 namespace {
 
+#ifdef MF_LEAF_TRACE
+// Diagnostic build only (-DMF_LEAF_TRACE): per-CTA timestamps (globaltimer, ns)
+// at entry, first data ready, end of the k loop and end of the epilogue, plus
+// the SM id -- where a tile's time goes outside the DMMA stream.
+constexpr int kTraceMax = 1 << 16;
+__device__ unsigned long long g_leaf_trace[kTraceMax][5];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(i) \
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) g_leaf_trace[blockIdx.x][i] = gtime()
+#else
+#define TRACE(i)
+#endif
+
 constexpr int BM = 128, BN = 128, BK = 16;  // BN: the default (widest) tile; BK: one k sub-block
 constexpr int MMA_WARPS = 8;
 constexpr int THREADS = MMA_WARPS * 32;
@@ -191,6 +208,14 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const int tm = prm.tm0 + first_m + (t % group_tiles) % gsz;
   const int tn = prm.tn0 + (t % group_tiles) / gsz;
   const LeafJob job = prm.jobs[job_id];
+  TRACE(0);
+#ifdef MF_LEAF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < kTraceMax) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_leaf_trace[blockIdx.x][4] = smid;
+  }
+#endif
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -287,6 +312,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   if (nk > 0) {
     mbar_wait(full0, 0);
+    TRACE(1);
     load_frags(s_base, s_base + A_BYTES, 0, fa0, fb0);
   }
   // fragment groups of the last stage that hold data: when m is not a
@@ -418,6 +444,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           }
       if (threadIdx.x == 0) prm.part_cnt[tail] = 0;  // ready for the next launch
     }
+    TRACE(2);
     // ---- epilogue: registers -> global (4 consecutive columns per thread) ----
     double* out = prm.out + (int64_t)job.out_idx * prm.out_stride;
     const double alpha = prm.alpha;
@@ -447,6 +474,7 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         }
       }
     }
+    TRACE(3);
   }
 }
 
@@ -541,6 +569,13 @@ bool encode_slot_view(CUtensorMap* map, const double* X, int slots, int64_t m, u
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
+
+#ifdef MF_LEAF_TRACE
+extern "C" int mf_debug_leaf_trace(unsigned long long* out, int n) {
+  n = n < kTraceMax ? n : kTraceMax;
+  return (int)cudaMemcpyFromSymbol(out, g_leaf_trace, sizeof(unsigned long long) * 5 * n);
+}
+#endif
 
 bool leaf_tma_supported(const LeafArgs& a) {
   // TMA: 16-byte aligned bases, strides multiple of 16 bytes (m, ld even).
