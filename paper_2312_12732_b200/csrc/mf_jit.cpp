@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -318,6 +319,27 @@ bool jit_compile(const std::string& src, const char* arch, std::vector<char>& cu
   return ok;
 }
 
+// Process-wide cache of compiled code, keyed by (architecture, source): plans
+// of the same triple (or the same batch tables) compile once per process.
+namespace {
+std::mutex g_cache_mu;
+std::map<std::string, std::vector<char>>& cache() {
+  static std::map<std::string, std::vector<char>> c;
+  return c;
+}
+bool cache_get(const std::string& src, const char* arch, std::vector<char>& cubin) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = cache().find(std::string(arch) + "\n" + src);
+  if (it == cache().end()) return false;
+  cubin = it->second;
+  return true;
+}
+void cache_put(const std::string& src, const char* arch, const std::vector<char>& cubin) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  cache()[std::string(arch) + "\n" + src] = cubin;
+}
+}  // namespace
+
 // Build the generated kernels of a plan's tables on the current device: the
 // sources compile in parallel host threads (NVRTC is thread-safe), the
 // modules load on the calling thread (its context is the plan's).  A table
@@ -345,8 +367,14 @@ int jit_build_all(const std::vector<JitJob>& jobs) {
     shapes[i] = jit_shape(*jb.t);
     if (shapes[i].vw == 0) continue;
     th.emplace_back([&, i, jb] {
+      const std::string src = jit_source(*jb.t, jb.in_P, jb.out_P, shapes[i]);
+      if (cache_get(src, arch, cubins[i])) {
+        ok[i] = 1;
+        return;
+      }
       std::string log;
-      ok[i] = jit_compile(jit_source(*jb.t, jb.in_P, jb.out_P, shapes[i]), arch, cubins[i], log);
+      ok[i] = jit_compile(src, arch, cubins[i], log);
+      if (ok[i]) cache_put(src, arch, cubins[i]);
     });
   }
   for (auto& t : th) t.join();
