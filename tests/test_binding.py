@@ -232,3 +232,24 @@ def test_jit_generator_compiles_without_gpu():
     with pytest.raises(mf.MfError) as e:
         mf.jit_compile_check(big, 0, 0)
     assert e.value.status == mf.MF_ERR_UNSUPPORTED
+
+
+def test_plan_accepts_sandwiched_triples():
+    """mf_plan's own Brent check (include/mf.h: exact for integer, dyadic-exact
+    for dyadic coefficients) accepts triples outside the catalog with general
+    coefficients (tests/sandwich.py) and rejects a corrupted one."""
+    from sandwich import sandwich, P2_INT, P2_DYADIC, P3_INT
+    for name, mats in (("strassen-winograd", P2_INT), ("strassen-winograd", P2_DYADIC),
+                       ("laderman", P3_INT)):
+        t = triples.get(name)
+        U, V, W = sandwich(t.U, t.V, t.W, t.p, *mats)
+        s = triples.Triple(f"{name}-sandwich", t.p, U, V, W)
+        for levels in (1, 2):
+            p = mf.Plan(s, levels, t.p ** levels * 8, host_only=True)
+            assert p.info()["n_products"] == t.R ** levels
+            p.close()
+        W = W.copy()
+        W[0, 0] += 1
+        with pytest.raises(mf.MfError) as e:
+            mf.Plan(triples.Triple("bad", t.p, U, V, W), 1, t.p * 8, host_only=True)
+        assert e.value.status == mf.MF_ERR_BAD_TRIPLE

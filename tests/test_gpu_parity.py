@@ -881,3 +881,62 @@ def test_host_async_stream_matches_sync(name, levels, n, kw):
         p.dgemm_host_async_ptr(ins[0][0].data_ptr(), n, ins[0][1].data_ptr(), n, outs[0].data_ptr(), n)
         assert (p.dgemm_host(Ai, Bi) == exact(Ai, Bi)).all()  # drains the async call first
         assert (outs[0].numpy() == 2.0 * refs[0]).all()
+
+
+# ---- triples outside the catalog (tests/sandwich.py): no compiled-in K4/K6 ----
+
+def _sandwich_pair(name, kind):
+    from sandwich import sandwich, P2_INT, P2_DYADIC, P3_INT
+    mats = {"int": P2_INT if name == SW else P3_INT, "dyadic": P2_DYADIC}[kind]
+    t = oracle.catalog(name)
+    U, V, W = sandwich(t.U, t.V, t.W, t.p, *mats)
+    return (oracle.Triple(f"{name}-{kind}", t.p, U, V, W),
+            triples.Triple(f"{name}-{kind}", t.p, U, V, W))
+
+
+@pytest.mark.parametrize("path", ["jit", "generic", "generic-terms"])
+@pytest.mark.parametrize("name,kind,levels,n", [(SW, "int", 1, 128), (SW, "int", 2, 256),
+                                                (SW, "dyadic", 2, 200), ("laderman", "int", 1, 96)])
+def test_sandwich_triple_mix_bit_exact(name, kind, levels, n, path, monkeypatch):
+    """A triple the library has no compiled-in kernels for, with coefficients
+    2, -3, 1/4 ... (tests/sandwich.py): its plan-time generated K4/K6 (`jit`,
+    the default) and the table-driven kernels are bitwise the oracle's
+    pre-/post-additions on random fp64 -- the general-coefficient terms
+    (multiply, then add) included."""
+    _mix_path(monkeypatch, path)
+    to1, tp = _sandwich_pair(name, kind)
+    to = oracle.kron_power(to1, levels)
+    A, B = mf_inputs.pair("uniform", n, 41)
+    with mf.Plan(tp, levels, n) as p:
+        info, pr = p.info(), p.products()
+        m = info["leaf_n"]
+        for side, X, src, idx in (("A", A, pr["a_src"], pr["a_idx"]), ("B", B, pr["b_src"], pr["b_idx"])):
+            nmat = info["n_mat_a"] if side == "A" else info["n_mat_b"]
+            out = torch.empty((max(nmat, 1), m, m), dtype=torch.float64, device="cuda")
+            p.premix(side, dev(X), out)
+            got, ref = host(out), oracle.premix(X, to, side)
+            for q in [q for q in range(to.R) if src[q] == 1]:
+                assert (got[idx[q]] == ref[q]).all(), (side, q)
+        rng = np.random.Generator(np.random.PCG64(43))
+        Pp = rng.uniform(-1, 1, size=(to.R, m, m))
+        sign = pr["sign"].astype(np.float64)
+        C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        p.postmix(dev(Pp), C, alpha=0.625)
+        assert (host(C) == oracle.postmix(Pp * sign[:, None, None], to, n, 0.625)).all()
+
+
+@pytest.mark.parametrize("path", ["jit", "generic"])
+@pytest.mark.parametrize("name,kind,levels,n", [(SW, "int", 2, 512), (SW, "dyadic", 2, 400),
+                                                ("laderman", "int", 1, 288)])
+def test_sandwich_triple_end_to_end(name, kind, levels, n, path, monkeypatch):
+    """End to end through mf_dgemm with a non-catalog triple: integer inputs
+    bit-exact with the exact product, random inputs within
+    1e-13 per level of the oracle's classical product."""
+    _mix_path(monkeypatch, path)
+    _, tp = _sandwich_pair(name, kind)
+    A, B = mf_inputs.pair("int8", n, 44)  # coefficients up to 4: keep partials < 2^53
+    with mf.Plan(tp, levels, n) as p:
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 45)
+        C = host(p.dgemm(dev(A), dev(B)))
+    assert scaled(C, oracle.classical(A, B), A, B) <= 1e-13 * levels

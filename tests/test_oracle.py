@@ -348,3 +348,45 @@ def test_sample_entries_match_classical():
     C = oracle.classical(A, B)
     rows = np.array([0, 5, 63, 17]); cols = np.array([3, 63, 0, 17])
     assert (oracle.sample_entries(A, B, rows, cols) == C[rows, cols]).all()
+
+
+# ---- triples outside the catalog (tests/sandwich.py): general coefficients ----
+
+def _sandwiched(name, mats):
+    from sandwich import sandwich
+    t = oracle.catalog(name)
+    return oracle.Triple(f"{name}-sandwich", t.p, *sandwich(t.U, t.V, t.W, t.p, *mats))
+
+
+def test_sandwich_triples_valid():
+    """A sandwich X A Y^-1, Y B Z^-1 of a valid triple is valid (tests/sandwich.py):
+    the integer ones pass the exact Brent check with coefficients up to 3 in
+    magnitude; the dyadic one (coefficients 1/4, 1/2, 4) is refused by the
+    integer check but reproduces exact products on scalar leaves (brute force,
+    n = p) and on integer matrices through two levels -- the interpreter's
+    general-coefficient terms (multiply, then add) are exercised."""
+    from sandwich import P2_INT, P2_DYADIC, P3_INT
+    rng = np.random.Generator(np.random.PCG64(77))
+    for name, mats, integral in (("strassen-winograd", P2_INT, True), ("laderman", P3_INT, True),
+                                 ("strassen-winograd", P2_DYADIC, False)):
+        s = _sandwiched(name, mats)
+        coefs = np.unique(np.concatenate([s.U.ravel(), s.V.ravel(), s.W.ravel()]))
+        assert np.abs(coefs).max() >= 2
+        if integral:
+            assert oracle.brent_check(s) == (0, None)
+        else:
+            with pytest.raises(ValueError):
+                oracle.brent_check(s)
+        for _ in range(10):
+            A = rng.integers(-9, 10, (s.p, s.p)).astype(np.float64)
+            B = rng.integers(-9, 10, (s.p, s.p)).astype(np.float64)
+            assert (oracle.fmm(A, B, s, 1) == A @ B).all()
+        n = s.p * s.p * 8
+        A = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
+        B = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
+        assert (oracle.fmm(A, B, s, 2) == oracle.classical(A, B)).all()
+    # a corrupted sandwich fails the exact check
+    s = _sandwiched("strassen-winograd", P2_INT)
+    W = s.W.copy()
+    W[0, 0] += 1
+    assert oracle.brent_check(oracle.Triple("bad", 2, s.U, s.V, W))[0] > 0
