@@ -511,7 +511,10 @@ def main():
                       "api": "mf_dgemm_host_async x K steps + mf_host_sync (pinned host A, B, C; "
                              "every step's H2D + compute + D2H inside the timed region; consecutive "
                              "steps overlap copies with compute"
-                             + (", per rank, NCCL reduce inside)" if distributed else ")"),
+                             + ("; product-sharded: each rank copies its 1/N row slab of A and B "
+                                "over its own PCIe link and NCCL all-gathers the rest over NVLink, "
+                                "the NCCL reduce of C runs inside, C returns to rank 0's host buffer)"
+                                if distributed else ")"),
                       "sync": {"value": 2.0 * n ** 3 / dts / 1e12, "ms_per_step": dts * 1e3,
                                "api": "mf_dgemm_host: one synchronous call per step"}}
         out["gpu_launches_e2e_per_step"] = launches_per_step(a)

@@ -72,6 +72,8 @@ struct Nccl {
                             cudaStream_t) = nullptr;
   ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
                                 ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -93,6 +95,7 @@ Nccl* nccl() {
     n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
     n.Broadcast = (decltype(n.Broadcast))dlsym(h, "ncclBroadcast");
     n.ReduceScatter = (decltype(n.ReduceScatter))dlsym(h, "ncclReduceScatter");
+    n.AllGather = (decltype(n.AllGather))dlsym(h, "ncclAllGather");
     n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
     n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
     n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
@@ -1345,8 +1348,35 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
   // every enqueued async call
   if ((!async || ns <= 1) && (st = host_drain(pl)) != MF_OK) return st;
   if (ns <= 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
-    MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
-    MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
+    const int N = pl->shard_count;
+    Nccl* nc = pl->nccl_comm ? nccl() : nullptr;
+    if (nc && nc->AllGather && n % N == 0 && pl->opt.input_mode == MF_IN_REPLICATED &&
+        !getenv("MF_HOST_FULLCOPY")) {
+      // product-sharded ranks with replicated host inputs: each rank copies
+      // its 1/N row slab of A and B over its own PCIe link, then NCCL
+      // all-gathers the slabs over NVLink (in place) -- the host traffic per
+      // GPU falls by N, the operand exchange is the NVLink collective
+      const int64_t rows = n / N, r0 = (int64_t)pl->shard_rank * rows;
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA + r0 * n, n * 8, A + r0 * lda, lda * 8, n * 8, rows,
+                                cudaMemcpyHostToDevice, s), "H2D A slab");
+      MF_CUDA(cudaMemcpy2DAsync(pl->hB + r0 * n, n * 8, B + r0 * ldb, ldb * 8, n * 8, rows,
+                                cudaMemcpyHostToDevice, s), "H2D B slab");
+      ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
+      ncclResult_t r;
+      if ((r = nc->GroupStart()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupStart");
+      if ((r = nc->AllGather(pl->hA + r0 * n, pl->hA, (size_t)rows * n, ncclDouble, comm, s)) != ncclSuccess) {
+        nc->GroupEnd();
+        return nccl_fail(nc, r, "ncclAllGather(A)");
+      }
+      if ((r = nc->AllGather(pl->hB + r0 * n, pl->hB, (size_t)rows * n, ncclDouble, comm, s)) != ncclSuccess) {
+        nc->GroupEnd();
+        return nccl_fail(nc, r, "ncclAllGather(B)");
+      }
+      if ((r = nc->GroupEnd()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupEnd");
+    } else {
+      MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
+      MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
+    }
     mf_options saved = pl->opt;
     pl->opt.input_mode = MF_IN_REPLICATED;
     st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
@@ -1354,7 +1384,10 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
     if (st != MF_OK) return st;
     const int64_t c_rows =
         pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB ? n / pl->shard_count : n;
-    MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, s), "D2H C");
+    // MF_OUT_ROOT: C is defined on rank 0 only -- the other ranks copy nothing back
+    const bool want_c = !(pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROOT && pl->shard_rank != 0);
+    if (want_c)
+      MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, s), "D2H C");
     MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return MF_OK;
   }

@@ -440,17 +440,23 @@ def test_nccl_single_rank_plan_matches_local():
     """The NCCL exchange step of the sharded path (mf_nccl_unique_id /
     mf_nccl_comm_create / reduce of C in mf_dgemm) on a 1-rank communicator:
     bitwise the local result; OUT_ALL (all-reduce) too; and IN_ROOT inputs are
-    broadcast into plan replicas."""
+    broadcast into plan replicas.  Through mf_dgemm_host too: with replicated
+    host inputs each rank copies its row slab and NCCL all-gathers the rest
+    (strided host views included); IN_ROOT copies everything."""
     n = 512
     A, B = mf_inputs.pair("uniform", n, 30)
     with mf.Plan(triples.get(SW), 2, n) as p:
         ref = host(p.dgemm(dev(A), dev(B)))
     comm = mf.nccl_comm_create(mf.nccl_unique_id(), 0, 1)
+    Aw = np.zeros((n, n + 8)); Aw[:, :n] = A
+    Bw = np.zeros((n, n + 16)); Bw[:, :n] = B
     try:
         for out_mode, in_mode in ((mf.OUT_ROOT, mf.IN_REPLICATED), (mf.OUT_ALL, mf.IN_ROOT)):
             with mf.Plan(triples.get(SW), 2, n, shard_rank=0, shard_count=1, nccl_comm=comm,
                          output_mode=out_mode, input_mode=in_mode) as p:
                 C = host(p.dgemm(dev(A), dev(B)))
+                assert (p.dgemm_host(A, B) == ref).all()
+                assert (p.dgemm_host(Aw[:, :n], Bw[:, :n]) == ref).all()
             assert (C == ref).all()
     finally:
         mf.nccl_comm_destroy(comm)
