@@ -1281,10 +1281,20 @@ static int pipeline_slabs(const Plan& pl) {
   if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
       !pl.batches.empty() || pl.fuse)
     return 1;
-  // 16 slabs of >= 2 tile rows each: the first region needs only 1/16 of A
-  // and B to land (n=16384 SW^2: sync call 202.7 -> 199.0 ms vs 8 slabs)
+  // as many slabs as keep every region launch above 1.3 waves of 128x128
+  // tiles (products x (tile rows per slab)^2 >= 1.3 SMs), up to 16 slabs
+  // of >= 2 tile rows: fewer bytes must land before the first region starts
+  // (n=16384 SW^2: sync call 202.7 -> 199.0 ms at 16 slabs vs 8), while a
+  // sub-wave region would leave SMs idle (n=16384 SW^1 at 16 slabs: 112 tiles)
   const int64_t tiles = (pl.m + 127) / 128;
-  int64_t want = std::max<int64_t>(2, std::min<int64_t>(16, tiles / 2));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl.device);
+  const int64_t prods = std::max<int64_t>(1, (int64_t)pl.my_prods.size());
+  int64_t want = 2;
+  for (int64_t ns = 16; ns >= 2; --ns) {
+    const int64_t per = tiles / ns;  // the smaller slabs
+    if (per >= 2 && 10 * prods * per * per >= 13 * (int64_t)sms) { want = ns; break; }
+  }
   if (const char* e = getenv("MF_HOST_SLABS")) want = std::max(2, atoi(e));
   return (int)std::min<int64_t>(want, tiles);
 }
