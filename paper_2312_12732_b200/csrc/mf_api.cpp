@@ -353,7 +353,8 @@ void free_plan(Plan* pl) {
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->comm_events) cudaEventDestroy(e);
-  for (cudaEvent_t e : {pl->set_free[0], pl->set_free[1], pl->compute_done})
+  for (cudaEvent_t e : {pl->set_free[0], pl->set_free[1], pl->compute_done, pl->ser_in[0],
+                        pl->ser_in[1], pl->ser_done[0], pl->ser_done[1]})
     if (e) cudaEventDestroy(e);
   for (auto& b : pl->batches) {
     for (void* p : {b.mixA.d_table, b.mixB.d_table, b.mixC.d_table})
@@ -1356,50 +1357,82 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
   if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B");
   if (!pl->hC && cudaMalloc(&pl->hC, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C");
   const int ns = pipeline_slabs(*pl);
-  // synchronous calls (and plans without the region pipeline) first finish
-  // every enqueued async call
-  if ((!async || ns <= 1) && (st = host_drain(pl)) != MF_OK) return st;
-  if (ns <= 1) {  // serial: H2D, mf_dgemm, D2H on the call's stream
+  // synchronous calls first finish every enqueued async call
+  if (!async && (st = host_drain(pl)) != MF_OK) return st;
+  if (ns <= 1) {
+    // whole-matrix path (sharded, level-by-level, fused, batched or cuBLAS-leaf
+    // plans): H2D, mf_dgemm, D2H.  Async calls alternate between two device
+    // sets on three streams, so call k+1's copies in and call k-1's copy out
+    // run under call k's compute; the compute stream orders the workspace.
+    const int set = async ? (int)(pl->async_calls & 1) : 0;
+    if (async) {
+      if (!pl->hA2 && cudaMalloc(&pl->hA2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device A (2nd set)");
+      if (!pl->hB2 && cudaMalloc(&pl->hB2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device B (2nd set)");
+      if (!pl->hC2 && cudaMalloc(&pl->hC2, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "device C (2nd set)");
+      for (cudaEvent_t* e : {&pl->set_free[0], &pl->set_free[1], &pl->ser_in[0], &pl->ser_in[1],
+                             &pl->ser_done[0], &pl->ser_done[1]})
+        if (!*e) MF_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+      for (cudaStream_t* q : {&pl->h2d, &pl->d2h, &pl->cs1})
+        if (!*q) MF_CUDA(cudaStreamCreateWithFlags(q, cudaStreamNonBlocking), "stream");
+    }
+    double* const dA = set ? pl->hA2 : pl->hA;
+    double* const dB = set ? pl->hB2 : pl->hB;
+    double* const dC = set ? pl->hC2 : pl->hC;
+    cudaStream_t cin = async ? pl->h2d : s, cc = async ? pl->cs1 : s, cout = async ? pl->d2h : s;
+    // a set is refilled once its previous call's copy out (after its compute) is done
+    if (async && pl->set_busy[set]) MF_CUDA(cudaStreamWaitEvent(cin, pl->set_free[set], 0), "wait");
     const int N = pl->shard_count;
     Nccl* nc = pl->nccl_comm ? nccl() : nullptr;
-    if (nc && nc->AllGather && n % N == 0 && pl->opt.input_mode == MF_IN_REPLICATED &&
-        !getenv("MF_HOST_FULLCOPY")) {
-      // product-sharded ranks with replicated host inputs: each rank copies
-      // its 1/N row slab of A and B over its own PCIe link, then NCCL
-      // all-gathers the slabs over NVLink (in place) -- the host traffic per
-      // GPU falls by N, the operand exchange is the NVLink collective
-      const int64_t rows = n / N, r0 = (int64_t)pl->shard_rank * rows;
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA + r0 * n, n * 8, A + r0 * lda, lda * 8, n * 8, rows,
-                                cudaMemcpyHostToDevice, s), "H2D A slab");
-      MF_CUDA(cudaMemcpy2DAsync(pl->hB + r0 * n, n * 8, B + r0 * ldb, ldb * 8, n * 8, rows,
-                                cudaMemcpyHostToDevice, s), "H2D B slab");
+    const bool slabs = nc && nc->AllGather && n % N == 0 && pl->opt.input_mode == MF_IN_REPLICATED &&
+                       !getenv("MF_HOST_FULLCOPY");
+    const int64_t rows = slabs ? n / N : n, r0 = slabs ? (int64_t)pl->shard_rank * rows : 0;
+    // product-sharded ranks with replicated host inputs copy only their 1/N
+    // row slab of A and B over their own PCIe link; NCCL all-gathers the rest
+    // over NVLink (in place) -- host traffic per GPU falls by N
+    MF_CUDA(cudaMemcpy2DAsync(dA + r0 * n, n * 8, A + r0 * lda, lda * 8, n * 8, rows,
+                              cudaMemcpyHostToDevice, cin), "H2D A");
+    MF_CUDA(cudaMemcpy2DAsync(dB + r0 * n, n * 8, B + r0 * ldb, ldb * 8, n * 8, rows,
+                              cudaMemcpyHostToDevice, cin), "H2D B");
+    if (async) {
+      MF_CUDA(cudaEventRecord(pl->ser_in[set], cin), "event");
+      MF_CUDA(cudaStreamWaitEvent(cc, pl->ser_in[set], 0), "wait");
+    }
+    if (slabs) {
       ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
       ncclResult_t r;
       if ((r = nc->GroupStart()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupStart");
-      if ((r = nc->AllGather(pl->hA + r0 * n, pl->hA, (size_t)rows * n, ncclDouble, comm, s)) != ncclSuccess) {
+      if ((r = nc->AllGather(dA + r0 * n, dA, (size_t)rows * n, ncclDouble, comm, cc)) != ncclSuccess) {
         nc->GroupEnd();
         return nccl_fail(nc, r, "ncclAllGather(A)");
       }
-      if ((r = nc->AllGather(pl->hB + r0 * n, pl->hB, (size_t)rows * n, ncclDouble, comm, s)) != ncclSuccess) {
+      if ((r = nc->AllGather(dB + r0 * n, dB, (size_t)rows * n, ncclDouble, comm, cc)) != ncclSuccess) {
         nc->GroupEnd();
         return nccl_fail(nc, r, "ncclAllGather(B)");
       }
       if ((r = nc->GroupEnd()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupEnd");
-    } else {
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D A");
-      MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyHostToDevice, s), "H2D B");
     }
     mf_options saved = pl->opt;
     pl->opt.input_mode = MF_IN_REPLICATED;
-    st = mf_dgemm(pl, alpha, pl->hA, n, pl->hB, n, pl->hC, n, stream);
+    st = mf_dgemm(pl, alpha, dA, n, dB, n, dC, n, cc);
     pl->opt = saved;
     if (st != MF_OK) return st;
+    if (async) {
+      MF_CUDA(cudaEventRecord(pl->ser_done[set], cc), "event");
+      MF_CUDA(cudaStreamWaitEvent(cout, pl->ser_done[set], 0), "wait");
+    }
     const int64_t c_rows =
         pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB ? n / pl->shard_count : n;
     // MF_OUT_ROOT: C is defined on rank 0 only -- the other ranks copy nothing back
     const bool want_c = !(pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROOT && pl->shard_rank != 0);
     if (want_c)
-      MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, pl->hC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, s), "D2H C");
+      MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, cout), "D2H C");
+    if (async) {
+      MF_CUDA(cudaEventRecord(pl->set_free[set], cout), "event");
+      pl->set_busy[set] = true;
+      MF_CUDA(cudaStreamWaitEvent(s, pl->set_free[set], 0), "wait");  // the caller's stream ends after it
+      ++pl->async_calls;
+      return MF_OK;
+    }
     MF_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
     return MF_OK;
   }

@@ -189,6 +189,8 @@ struct Plan {
   cudaEvent_t set_free[2] = {nullptr, nullptr};
   bool set_busy[2] = {false, false};
   cudaEvent_t compute_done = nullptr;
+  cudaEvent_t ser_in[2] = {nullptr, nullptr};    // whole-matrix async path: inputs landed
+  cudaEvent_t ser_done[2] = {nullptr, nullptr};  // ... and computed
   bool compute_pending = false;
   cudaStream_t cs1 = nullptr;
   int64_t async_calls = 0;
