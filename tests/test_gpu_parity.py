@@ -585,13 +585,20 @@ def _sampled_check(C, A, B, count=256, seed=0, tol=None):
 
 
 @pytest.mark.parametrize("name,levels,n", [(SW, 1, 4096), (SW, 2, 16384), ("laderman", 1, 13824),
-                                           (SW, 2, 13824), (SW, 2, 32768), (SW, 3, 16384)])
+                                           (SW, 2, 13824), (SW, 2, 32768), (SW, 3, 16384),
+                                           ("laderman", 2, 13824), (SW + "(x)laderman", 1, 13824),
+                                           ("laderman(x)" + SW, 1, 13824)])
 def test_bench_configs_full_size(name, levels, n):
     """BASELINE configs 2-5 at full size (config 5: its 1-GPU problem, n=32768,
-    69 GB of workspace) and the bench's SW^3 variant, in the launch
-    configuration bench.py times (k = 48 leaf stages at m = 3456, 4608, 8192):
-    exact Freivalds on integers + sampled oracle entries on random."""
-    t = triples.get(name)
+    69 GB of workspace) and the reported variants (SW^3, Laderman^2, both mixed
+    chains <6,6,6;161>), in the launch configuration bench.py times (k = 48 leaf
+    stages at m = 3456, 4608, 8192; 2304 for the chains): exact Freivalds on
+    integers + sampled oracle entries on random."""
+    if "(x)" in name:
+        o, i = name.split("(x)")
+        t = triples.kron(triples.get(o), triples.get(i))
+    else:
+        t = triples.get(name)
     with mf.Plan(t, levels, n) as p:
         Ad, Bd = mf_inputs.device_pair("int1024", n, 21)
         C = host(p.dgemm(Ad, Bd))
