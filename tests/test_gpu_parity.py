@@ -362,6 +362,27 @@ def test_sw4_hybrid_bench_size_sampled():
     _sampled_check(C, A, B, count=128, tol=4e-13)
 
 
+def test_sw5_hybrid_full_size():
+    """The five-level preset at full size (n = 32768: two SW levels one at a
+    time over 49 flattened SW^3 children at n = 8192, 16807 leaves of 1024^2):
+    exact Freivalds on integers (entries in [-8, 8]: every partial sum of five
+    levels stays below 2^53, DESIGN R15), sampled oracle entries on random
+    inputs within 1e-13 per level."""
+    n = 32768
+    with mf.Plan(triples.get(SW), 5, n, level_by_level=True, recurse_levels=2) as p:
+        Ad, Bd = mf_inputs.device_pair("int8", n, 50)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+        del Ad, Bd
+        assert oracle.freivalds_int(A, B, C, trials=2) == 0
+        _sampled_check(C, A, B, count=64)
+        del A, B, C
+        Ad, Bd = mf_inputs.device_pair("uniform", n, 51)
+        C = host(p.dgemm(Ad, Bd))
+        A, B = host(Ad), host(Bd)
+    _sampled_check(C, A, B, count=64, tol=5e-13)
+
+
 def test_config1_n64_sw1_all_distributions():
     """BASELINE config 1: n=64, one-level Strassen-Winograd."""
     for kind in ("int8", "int1024"):
