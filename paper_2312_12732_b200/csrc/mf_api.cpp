@@ -342,7 +342,8 @@ void free_plan(Plan* pl) {
                   (void*)pl->mixB.d_table, (void*)pl->mixC.d_table, (void*)pl->mixA2.d_table,
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
-                  (void*)pl->split_ws, (void*)pl->split_cnt, (void*)pl->hA2, (void*)pl->hB2,
+                  (void*)pl->split_ws, (void*)pl->split_cnt, (void*)pl->d_tinyU, (void*)pl->d_tinyV,
+                  (void*)pl->d_tinyW, (void*)pl->hA2, (void*)pl->hB2,
                   (void*)pl->hC2,
                   (void*)pl->hC})
     if (p) cudaFree(p);
@@ -797,6 +798,16 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       free_plan(pl.get());
       return st;
     }
+    // small problems run the whole level as one cluster launch (mf_tiny.cu)
+    if (levels > 0 && n <= 64 && pl->RL <= 64) {
+      const size_t tb2 = sizeof(double) * pl->U.size();
+      bool ok = cudaMalloc(&pl->d_tinyU, tb2) == cudaSuccess && cudaMalloc(&pl->d_tinyV, tb2) == cudaSuccess &&
+                cudaMalloc(&pl->d_tinyW, tb2) == cudaSuccess;
+      ok = ok && cudaMemcpy(pl->d_tinyU, pl->U.data(), tb2, cudaMemcpyHostToDevice) == cudaSuccess &&
+           cudaMemcpy(pl->d_tinyV, pl->V.data(), tb2, cudaMemcpyHostToDevice) == cudaSuccess &&
+           cudaMemcpy(pl->d_tinyW, pl->W.data(), tb2, cudaMemcpyHostToDevice) == cudaSuccess;
+      if (!ok) { free_plan(pl.get()); return fail(MF_ERR_OUT_OF_MEMORY, "small-problem tables"); }
+    }
     // triples without compiled-in K4/K6, and the local tables of batches:
     // generate and compile their kernels now (mf_jit.cpp)
     std::vector<JitJob> jj;
@@ -1054,7 +1065,12 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
   bool reduced = false;  // C already summed over ranks region by region
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
   mark(0);
-  if (pl->levels == 0) {
+  if (tiny_eligible(*pl) && !getenv("MF_TINY_OFF")) {
+    // n <= 64: the whole level in one cluster launch (profile: the leaf phase)
+    mark(1); mark(2);
+    MF_CUDA(launch_tiny(*pl, alpha, A, lda, B, ldb, C, ldc, s), "small-problem kernel");
+    mark(3);
+  } else if (pl->levels == 0) {
     mark(1); mark(2);
     if ((st = run_leaf(*pl, A, lda, B, ldb, nullptr, nullptr, C, ldc, 0, alpha, s)) != MF_OK) return st;
     mark(3);

@@ -156,6 +156,10 @@ struct Plan {
   PostTerm* d_post = nullptr;
   size_t ws_bytes = 0;
   LeafJob* d_jobs = nullptr;  // my_prods.size() jobs
+  // small problems (mf_tiny.cu): the flattened U, V, W on the device
+  double* d_tinyU = nullptr;
+  double* d_tinyV = nullptr;
+  double* d_tinyW = nullptr;
   std::vector<LeafJob> h_jobs;  // host copy (MF_LEAF_CUBLAS builds pointer arrays from it)
   void* cublas = nullptr;       // cublasHandle_t (MF_LEAF_CUBLAS), created on first use
   const double** d_ptrs = nullptr;  // device pointer arrays for cublasDgemmBatched
@@ -263,6 +267,10 @@ struct LeafArgs {
   int64_t split_cnt_len = 0;
 };
 bool leaf_tma_supported(const LeafArgs& a);
+// mf_tiny.cu: one cluster launch for a whole small level (n <= 64, R^L <= 64)
+bool tiny_eligible(const Plan& pl);
+cudaError_t launch_tiny(const Plan& pl, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double* C, int64_t ldc, cudaStream_t s);
 // tile width and split-K tail chosen for a DMMA leaf launch (mf_leaf.cu)
 struct LeafTiles {
   int bn = 128;

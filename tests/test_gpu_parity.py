@@ -996,3 +996,40 @@ def test_sandwich_triple_end_to_end(name, kind, levels, n, path, monkeypatch):
         A, B = mf_inputs.pair("uniform", n, 45)
         C = host(p.dgemm(dev(A), dev(B)))
     assert scaled(C, oracle.classical(A, B), A, B) <= 1e-13 * levels
+
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 1, 64), (SW, 2, 64), ("laderman", 1, 36),
+                                           ("paper-strassen", 2, 32), ("strassen-1969", 1, 8),
+                                           (SW, 3, 64), ("classical-p2", 1, 16)])
+def test_tiny_single_launch(name, levels, n, monkeypatch):
+    """n <= 64, R^L <= 64: the whole level as one thread-block cluster launch
+    (mf_tiny.cu: pre-additions, products and post-additions, the products read
+    across the cluster through distributed shared memory).  Integer inputs:
+    bit-exact with the exact product; random: within the bound of the oracle,
+    and equal to the four-launch path to rounding (the leaf dot products are
+    fma chains in both, in different k orders); alpha applied last; graph
+    replay bitwise the eager call."""
+    t = triples.get(name)
+    A, B = mf_inputs.pair("int1024", n, 60)
+    with mf.Plan(t, levels, n) as p:
+        assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all()
+        assert (host(p.dgemm(dev(A), dev(B), alpha=-3.0)) == -3.0 * exact(A, B)).all()
+        A, B = mf_inputs.pair("uniform", n, 61)
+        Ct = host(p.dgemm(dev(A), dev(B), alpha=0.75))
+    monkeypatch.setenv("MF_TINY_OFF", "1")
+    with mf.Plan(t, levels, n) as p:
+        Cg = host(p.dgemm(dev(A), dev(B), alpha=0.75))
+    monkeypatch.delenv("MF_TINY_OFF")
+    ref = 0.75 * oracle.fmm(A, B, oracle.catalog(name), levels)
+    assert scaled(Ct, ref, A, B) <= 1e-13 * levels
+    assert scaled(Ct, Cg, A, B) <= 1e-13 * levels
+    s = torch.cuda.Stream()
+    with mf.Plan(t, levels, n, graph=True) as p, torch.cuda.stream(s):
+        Ad, Bd = dev(A), dev(B)
+        C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+        outs = []
+        for _ in range(3):  # eager, capture, replay
+            p.dgemm(Ad, Bd, C, stream=s)
+            s.synchronize()
+            outs.append(host(C).copy())
+    assert (outs[0] == outs[1]).all() and (outs[0] == outs[2]).all()
