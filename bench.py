@@ -146,6 +146,9 @@ def launches_per_step(a):
     child calls."""
     if a.levels == 0:
         return 1
+    if (a.n <= 64 and _rank(a) ** a.levels <= 64 and not a.fuse and not a.level_by_level
+            and a.leaf == "dmma" and not a.max_workspace_gb and not os.environ.get("MF_TINY_OFF")):
+        return 1  # the whole level as one cluster launch (mf_tiny.cu)
     flat = 3 if a.fuse else 4
     if not a.level_by_level or a.levels < 2:
         return flat
