@@ -814,6 +814,11 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     if (pl->fixed_id == 0 && levels > 0) {
       for (MixTable* t : {&pl->mixA, &pl->mixA2, &pl->mixB}) jj.push_back({t, pl->P, 0});
       for (MixTable* t : {&pl->mixC, &pl->mixC2}) jj.push_back({t, 0, pl->P});
+    } else if (levels > 0 && pl->fixed_id < 8 && shard_count > 1 && !getenv("MF_SHARD_MASKED")) {
+      // a shard's K4 over its own slots only: the generated kernel reads just
+      // the input blocks those slots use (the masked compiled-in kernel
+      // streams all of them); same flat ascending order, so bitwise the same
+      for (MixTable* t : {&pl->mixA, &pl->mixA2, &pl->mixB}) jj.push_back({t, pl->P, 0});
     }
     for (auto& b : pl->batches) {
       jj.push_back({&b.mixA, pl->P, 0});

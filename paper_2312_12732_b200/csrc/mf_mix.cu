@@ -335,6 +335,10 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
   // selects the outputs (A: whole products, or split products on their rows)
   const bool own = &t == &pl.mixA || &t == &pl.mixA2 || &t == &pl.mixB;
   if (pl.fixed_id > 0 && own) {
+    if (pl.shard_count > 1 && t.jit_fn) {  // a shard's own slots (see mf_plan)
+      const cudaError_t j = jit_launch(t, X, ldx, out, pl.m, pl.m, 1.0, rows, 0, s);
+      if (j != cudaErrorNotSupported) return j;
+    }
     const int side = &t == &pl.mixB ? 1 : 0;
     const ProdMask& mask = &t == &pl.mixA ? pl.mask_whole : (&t == &pl.mixA2 ? pl.mask_part : pl.mask_all);
     if (pl.fixed_id >= 8) return launch_premix_kron(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
