@@ -390,3 +390,32 @@ def test_sandwich_triples_valid():
     W = s.W.copy()
     W[0, 0] += 1
     assert oracle.brent_check(oracle.Triple("bad", 2, s.U, s.V, W))[0] > 0
+
+
+def test_random_sandwiches_stay_valid():
+    """Property: for random unimodular X, Y, Z (products of elementary integer
+    matrices), the sandwich of a valid triple is valid -- exact Brent check,
+    and the interpreter reproduces exact products on scalar leaves.  A dropped
+    or mis-indexed term anywhere in or_brent_check / or_fmm's combination
+    code would break one of these on some draw."""
+    from sandwich import sandwich
+    rng = np.random.Generator(np.random.PCG64(2024))
+
+    def unimodular(p):
+        M = np.eye(p, dtype=np.int64)
+        for _ in range(3):
+            i, j = rng.choice(p, 2, replace=False)
+            E = np.eye(p, dtype=np.int64)
+            E[i, j] = rng.choice([-1, 1])
+            M = M @ E
+        return M
+
+    for name in ("strassen-winograd", "laderman", "strassen-1969"):
+        t = oracle.catalog(name)
+        for _ in range(6):
+            s = oracle.Triple("s", t.p, *sandwich(t.U, t.V, t.W, t.p, unimodular(t.p),
+                                                  unimodular(t.p), unimodular(t.p)))
+            assert oracle.brent_check(s) == (0, None)
+            A = rng.integers(-9, 10, (t.p, t.p)).astype(np.float64)
+            B = rng.integers(-9, 10, (t.p, t.p)).astype(np.float64)
+            assert (oracle.fmm(A, B, s, 1) == A @ B).all()
