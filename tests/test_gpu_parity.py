@@ -1033,3 +1033,46 @@ def test_tiny_single_launch(name, levels, n, monkeypatch):
             s.synchronize()
             outs.append(host(C).copy())
     assert (outs[0] == outs[1]).all() and (outs[0] == outs[2]).all()
+
+
+def test_random_sandwich_triples_generated_kernels_bit_exact():
+    """Property over random unimodular block transforms of SW and Laderman
+    (tests/sandwich.py): each draw is a fresh triple, so each plan generates and
+    compiles new K4/K6; pre- and post-additions bitwise the oracle's, the
+    integer product exact."""
+    from sandwich import sandwich
+    rng = np.random.Generator(np.random.PCG64(77))
+
+    def unimodular(p):
+        M = np.eye(p, dtype=np.int64)
+        for _ in range(3):
+            i, j = rng.choice(p, 2, replace=False)
+            E = np.eye(p, dtype=np.int64)
+            E[i, j] = rng.choice([-1, 1])
+            M = M @ E
+        return M
+
+    for name, n in ((SW, 128), ("laderman", 96), (SW, 256)):
+        t = oracle.catalog(name)
+        for _ in range(2):
+            U, V, W = sandwich(t.U, t.V, t.W, t.p, unimodular(t.p), unimodular(t.p), unimodular(t.p))
+            to, tp = oracle.Triple("s", t.p, U, V, W), triples.Triple("s", t.p, U, V, W)
+            A, B = mf_inputs.pair("uniform", n, int(rng.integers(1 << 30)))
+            with mf.Plan(tp, 1, n) as p:
+                info, pr = p.info(), p.products()
+                m = info["leaf_n"]
+                for side, X, src, idx in (("A", A, pr["a_src"], pr["a_idx"]),
+                                          ("B", B, pr["b_src"], pr["b_idx"])):
+                    nmat = info["n_mat_a"] if side == "A" else info["n_mat_b"]
+                    out = torch.empty((max(nmat, 1), m, m), dtype=torch.float64, device="cuda")
+                    p.premix(side, dev(X), out)
+                    got, ref = host(out), oracle.premix(X, to, side)
+                    for q in [q for q in range(to.R) if src[q] == 1]:
+                        assert (got[idx[q]] == ref[q]).all()
+                Pp = rng.uniform(-1, 1, size=(to.R, m, m))
+                sign = pr["sign"].astype(np.float64)
+                C = torch.empty((n, n), dtype=torch.float64, device="cuda")
+                p.postmix(dev(Pp), C, alpha=1.0)
+                assert (host(C) == oracle.postmix(Pp * sign[:, None, None], to, n, 1.0)).all()
+                Ai, Bi = mf_inputs.pair("int8", n, 5)
+                assert (host(p.dgemm(dev(Ai), dev(Bi))) == exact(Ai, Bi)).all()
