@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--levels", type=int, default=2)
     ap.add_argument("--Ns", default="2,4,8")
+    ap.add_argument("--regions", type=int, default=0,
+                    help="comm_regions of the real multi-GPU run (8 by default there); 0 = one launch")
     a = ap.parse_args()
     n = a.n
     A, B = mf_inputs.device_pair("uniform", n, 0, device="cuda:0")
@@ -50,11 +52,12 @@ def main():
     for N in (int(x) for x in a.Ns.split(",")):
         per = []
         for r in range(N):
-            with mf.Plan(t, a.levels, n, device=0, shard_rank=r, shard_count=N) as p:
+            with mf.Plan(t, a.levels, n, device=0, shard_rank=r, shard_count=N,
+                         comm_regions=a.regions) as p:
                 per.append(step_ms(p, A, B, C))
             torch.cuda.empty_cache()
         tmax = max(per)
-        print(json.dumps({"n": n, "N": N, "rank_ms": [round(x, 3) for x in per], "max_ms": tmax,
+        print(json.dumps({"n": n, "N": N, "regions": a.regions, "rank_ms": [round(x, 3) for x in per], "max_ms": tmax,
                           "tflops_compute_only": fl / tmax / 1e9,
                           "efficiency_vs_1gpu": t1 / (N * tmax)}), flush=True)
 
