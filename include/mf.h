@@ -169,7 +169,13 @@ mf_status mf_dgemm(mf_plan_t plan, double alpha, const double* A, int64_t lda,
 
 /* mf_dgemm_host -- the same product with HOST A, B, C (any host memory;
  * pinned memory is fastest).  Copies A and B to plan-owned device buffers,
- * runs mf_dgemm, copies C back; returns after C is complete on the host. */
+ * runs mf_dgemm, copies C back; returns after C is complete on the host.
+ * Single-GPU flattened plans pipeline the copies with the compute by row /
+ * column slabs.  Sharded plans with an NCCL communicator and
+ * MF_IN_REPLICATED inputs copy only their 1/N row slab of A and B and
+ * all-gather the rest over NVLink (every rank must pass the full host A, B);
+ * with MF_OUT_ROOT only rank 0 copies C back, with MF_OUT_ROWSLAB each rank
+ * its slab. */
 mf_status mf_dgemm_host(mf_plan_t plan, double alpha, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
@@ -181,9 +187,11 @@ mf_status mf_dgemm_host(mf_plan_t plan, double alpha, const double* A, int64_t l
  * bitwise those of mf_dgemm_host.  A and B must stay unchanged and C unread
  * until mf_host_sync (or a synchronisation of `stream`, which waits for the
  * call's last copy) returns; pinned host memory is needed for the overlap.
- * Plans without the region pipeline (sharded, NCCL, level-by-level, batched,
- * fused, non-DMMA leaf) run the call synchronously.  A later synchronous call
- * on the plan first waits for all enqueued async calls. */
+ * Plans without the slab pipeline (sharded, NCCL, level-by-level, batched,
+ * fused, non-DMMA leaf) stream whole matrices the same way (copy in, compute,
+ * copy out on three streams); the fused plan's results equal the synchronous
+ * call's to rounding (its bulk reductions add in a run-dependent order).  A
+ * later synchronous call on the plan first waits for all enqueued async calls. */
 mf_status mf_dgemm_host_async(mf_plan_t plan, double alpha, const double* A, int64_t lda,
                               const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
