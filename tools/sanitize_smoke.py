@@ -1,7 +1,8 @@
 """Small workloads touching every kernel path, for compute-sanitizer runs
 (memcheck / racecheck / synccheck, one tool per call):
-flattened + Kronecker-factored + generic K4/K6, leaf BN=128/64 and the simple
-leaf, ragged and odd sizes, host pipeline, level-by-level, sharded plans."""
+flattened + Kronecker-factored + generated + table-driven K4/K6, leaf BN=128/64
+and the simple leaf, the small-problem cluster kernel, ragged and odd sizes,
+bounded-workspace batches, host pipeline, level-by-level, sharded plans."""
 import os
 import sys
 
@@ -35,8 +36,14 @@ run(T.STRASSEN_WINOGRAD, 3, 256)         # Kronecker-factored K4/K6
 run(T.LADERMAN, 1, 288)
 run(T.LADERMAN, 2, 144)                  # factored, p=3
 os.environ["MF_MIX_GENERIC"] = "1"
-run(T.STRASSEN_WINOGRAD, 2, 256)         # generic table-driven K4/K6
+run(T.STRASSEN_WINOGRAD, 2, 256)         # plan-time generated K4/K6 (NVRTC)
+os.environ["MF_MIX_NOJIT"] = "1"
+run(T.STRASSEN_WINOGRAD, 2, 256)         # table-driven K4/K6 (grouped / term lists)
+del os.environ["MF_MIX_NOJIT"]
 del os.environ["MF_MIX_GENERIC"]
+run(T.STRASSEN_WINOGRAD, 1, 64)          # small problem: one cluster launch (DMMA, DSMEM pushes)
+run(T.LADERMAN, 1, 36)                   # small problem, fma leaf (m = 12)
+run(T.STRASSEN_WINOGRAD, 2, 512, max_workspace=3 * 5 * 128 * 128 * 8)  # batches
 run(T.STRASSEN_WINOGRAD, 2, 1024, host=True)   # host pipeline (regions, 4 streams)
 run(T.STRASSEN_WINOGRAD, 2, 256, level_by_level=True)
 n = 1024
