@@ -424,13 +424,35 @@ def main():
         leaf_flops = R ** a.levels * 2.0 * (n // p ** a.levels) ** 3
     peak, peak_src = fp64_peak()
     achieved = leaf_flops / (leaf_ms * 1e-3) / 1e12
+    # the leaf's algorithmic DRAM bytes: every distinct operand block (materialised
+    # slot or aliased input block) read once, every product written once
+    pr = plan.products()
+    mine = [q for q, sh in enumerate(shard) if sh == rank or sh == -1]
+    alg_bytes = None
+    if not a.level_by_level:
+        blk = 8.0 * m * m
+        ops_a = {(int(pr["a_src"][q]), int(pr["a_idx"][q])) for q in mine}
+        ops_b = {(int(pr["b_src"][q]), int(pr["b_idx"][q])) for q in mine}
+        alg_bytes = (len(ops_a) + len(ops_b) + len(mine)) * blk
     kernel = {"dmma": "leaf_dmma_kernel (K5)", "cublas": "cublasDgemmBatched leaf (ablation)",
               "simple": "leaf_simple_kernel (ablation)"}[a.leaf]
+    # ncu's leaf DRAM bytes (profiles/ncu_leaf.json) were captured on the default
+    # workload: reported only for it
+    default_wl = (a.n == 16384 and a.levels == 2 and a.triple == "strassen-winograd"
+                  and not a.fuse and not a.level_by_level and a.leaf == "dmma" and world == 1)
+    traffic = leaf_traffic() if default_wl else None
     roofline = {"bound": "tensor", "kernel": kernel, "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": leaf_traffic(),
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src, "flops_per_launch": leaf_flops, "ms_per_launch": leaf_ms,
                 "phase_ms_per_step": {k: phases[k] / max(1, phases["calls"]) for k in plan.PHASES},
-                "leaf_share_of_step": leaf_ms / ms}
+                "leaf_share_of_step": leaf_ms / ms,
+                "algorithmic_bytes": alg_bytes,
+                "traffic_over_algorithmic": traffic / alg_bytes if traffic and alg_bytes else None,
+                "traffic_note": ("ncu DRAM bytes of the leaf (profiles/ncu_leaf.json) over its "
+                                 "algorithmic bytes: B panels are re-read once per 8-tile-row "
+                                 "group because a 134 MB operand block does not stay in the "
+                                 "126 MB L2; the kernel is DMMA-bound at ~3% of HBM bandwidth "
+                                 "(DESIGN.md §5)")}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
