@@ -163,6 +163,17 @@ mf_status brent_check(int p, int R, const double* U, const double* V, const doub
     Vi[i] = (int64_t)std::ldexp(V[i], dexp[1]);
     Wi[i] = (int64_t)std::ldexp(W[i], dexp[2]);
   }
+  // every sum of R terms |U'V'W'| must stay inside __int128 (signed overflow
+  // would be undefined and could accept a wrong triple)
+  {
+    double mx[3] = {0, 0, 0};
+    const std::vector<int64_t>* sc[3] = {&Ui, &Vi, &Wi};
+    for (int t = 0; t < 3; ++t)
+      for (int64_t x : *sc[t]) mx[t] = std::max(mx[t], std::fabs((double)x));
+    if (mx[0] * mx[1] * mx[2] * (double)R >= std::ldexp(1.0, 125))
+      return fail(MF_ERR_UNSUPPORTED,
+                  "coefficients too large for the exact Brent check (scaled |U||V||W|R >= 2^125)");
+  }
   const __int128 one = (__int128)1 << (dexp[0] + dexp[1] + dexp[2]);
   int64_t bad = 0;
   int fx = -1, fy = -1, fz = -1;
@@ -682,9 +693,13 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     pl->fixed_id = fixed_match(*pl);
     if (pl->fixed_id == 0) pl->fixed_id = kron_match(*pl);
   }
-  for (int32_t q : pl->my_prods) pl->mask_whole.w[q >> 6] |= 1ull << (q & 63);
-  for (int32_t q : pl->my_part) pl->mask_part.w[q >> 6] |= 1ull << (q & 63);
-  for (int i = 0; i < 9; ++i) pl->mask_all.w[i] = pl->mask_whole.w[i] | pl->mask_part.w[i];
+  // the masks exist for the specialised K4/K6 only (RL <= 576 = 9 x 64 bits;
+  // larger flattened plans run generated or table kernels and leave them empty)
+  if (RL <= 64 * (int64_t)(sizeof(ProdMask::w) / sizeof(uint64_t))) {
+    for (int32_t q : pl->my_prods) pl->mask_whole.w[q >> 6] |= 1ull << (q & 63);
+    for (int32_t q : pl->my_part) pl->mask_part.w[q >> 6] |= 1ull << (q & 63);
+    for (int i = 0; i < 9; ++i) pl->mask_all.w[i] = pl->mask_whole.w[i] | pl->mask_part.w[i];
+  }
 
   // ---- mix tables for this shard ----
   auto add_slots = [&](MixTable& t, int side, const std::vector<int32_t>& qs) {
@@ -864,7 +879,12 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       free_plan(pl.get());
       return fail(MF_ERR_OUT_OF_MEMORY, "job table");
     }
-    cudaMemcpy(pl->d_jobs, jobs.data(), sizeof(LeafJob) * jobs.size(), cudaMemcpyHostToDevice);
+    const cudaError_t e = cudaMemcpy(pl->d_jobs, jobs.data(), sizeof(LeafJob) * jobs.size(),
+                                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(pl.get());
+      return cuda_fail(e, "upload job table");
+    }
   }
   pl->h_jobs = jobs;
   if (pl->fuse) {
@@ -891,9 +911,14 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       free_plan(pl.get());
       return fail(MF_ERR_OUT_OF_MEMORY, "fused post-addition table");
     }
-    cudaMemcpy(pl->d_post_off, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice);
-    if (!terms.empty())
-      cudaMemcpy(pl->d_post, terms.data(), sizeof(PostTerm) * terms.size(), cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpy(pl->d_post_off, off.data(), sizeof(int32_t) * off.size(),
+                               cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !terms.empty())
+      e = cudaMemcpy(pl->d_post, terms.data(), sizeof(PostTerm) * terms.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(pl.get());
+      return cuda_fail(e, "upload fused post-addition table");
+    }
   }
   if (cudaEventCreateWithFlags(&pl->done, cudaEventDisableTiming) != cudaSuccess) {
     free_plan(pl.get());

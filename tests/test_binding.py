@@ -253,3 +253,31 @@ def test_plan_accepts_sandwiched_triples():
         with pytest.raises(mf.MfError) as e:
             mf.Plan(triples.Triple("bad", t.p, U, V, W), 1, t.p * 8, host_only=True)
         assert e.value.status == mf.MF_ERR_BAD_TRIPLE
+
+
+@pytest.mark.parametrize("levels,shards", [(4, 1), (4, 8), (5, 3)])
+def test_flattened_plan_beyond_mask_capacity(levels, shards):
+    """Flattened plans with more than 576 products (SW^4: 2401, SW^5: 16807)
+    plan, report their products and close cleanly (the specialised kernels'
+    product mask holds 576 bits; larger plans must not touch it)."""
+    t = triples.STRASSEN_WINOGRAD
+    n = 2 ** levels * 8
+    p = mf.Plan(t, levels, n, host_only=True, shard_count=shards, shard_rank=shards - 1)
+    info = p.info()
+    assert info["n_products"] == 7 ** levels
+    sh = p.products()["shard"]
+    assert sh.max() == shards - 1 and (sh >= -1).all()
+    p.close()
+
+
+def test_brent_check_rejects_coefficients_beyond_exact_range():
+    """Dyadic coefficients whose scaled products could overflow the exact
+    __int128 check are refused (MF_ERR_UNSUPPORTED), not silently wrapped."""
+    t = triples.STRASSEN_WINOGRAD
+    # each entry passes on its own (|x 2^d| <= 1e6), but a 2^-30 entry scales the
+    # whole matrix by 2^30, so 9e5 becomes ~2^50 and U'V'W' ~2^150
+    U, V, W = (x * 9e5 for x in (t.U, t.V, t.W))
+    for M in (U, V, W):
+        M[M == 0] = 2.0 ** -30
+    st, msg = _plan_status(2, 7, U, V, W, 1, 64, host_only=1)
+    assert st == mf.MF_ERR_UNSUPPORTED and "exact Brent" in msg
