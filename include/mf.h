@@ -64,18 +64,27 @@ typedef struct {
                            libcublas.so.12 is dlopen'ed, MF_ERR_CUDA if absent;
                            not with fuse_postadd)                              */
   int32_t shard_rank;   /* product sharding: this rank's index (default 0)        */
-  int32_t shard_count;  /* number of shards; 0/1 = unsharded.  With nccl_comm ==
-                           NULL a sharded plan computes only its shard's PARTIAL C
-                           (used to emulate rank r of N on one GPU)               */
-  void* nccl_comm;      /* ncclComm_t from mf_nccl_comm_create, or NULL           */
+  int32_t shard_count;  /* number of shards; 0/1 = unsharded.  With comm == NULL
+                           a sharded plan computes only its shard's PARTIAL C
+                           (used to emulate rank r of N on one GPU).  With a
+                           communicator, shard_rank / shard_count must equal its
+                           rank / size (else MF_ERR_INVALID_ARG)              */
+  void* comm;           /* communicator handle from mf_nccl_comm_create (NCCL,
+                           one process per GPU) or mf_loop_comm_create (ranks
+                           as threads of one process), or NULL = one rank     */
   int32_t input_mode;   /* MF_IN_REPLICATED (inputs valid on every rank) or
-                           MF_IN_ROOT (rank 0's A, B are broadcast first)         */
+                           MF_IN_ROOT (only rank 0's A, B are read; the other
+                           ranks may pass NULL and receive them by broadcasts
+                           of row slabs, each slab's K4 starting as soon as it
+                           landed; rank 0 sends in place from A and B when
+                           lda == ldb == n, else from a packed copy)         */
   int32_t output_mode;  /* MF_OUT_ROOT (C summed onto rank 0), MF_OUT_ALL (C
                            summed onto every rank) or MF_OUT_ROWSLAB (rank r
                            receives rows [r*n/N, (r+1)*n/N) of the sum; its C
                            argument is that n/N x n slab, ldc == n; needs
                            n % N == 0; the full partial C lives in a
-                           plan-owned buffer).  Only with nccl_comm           */
+                           plan-owned buffer).  Only with comm; every mode
+                           needs ldc == n                                     */
   int32_t profile;      /* 1: mf_dgemm records CUDA events around each phase on
                            the call's stream (read with mf_profile_read)          */
   int32_t host_only;    /* 1: plan the host logic only (Brent check, flattening,
@@ -117,14 +126,17 @@ typedef struct {
                            configs are host-issue bound).  Ignored on the
                            legacy default stream (NULL) and with profile,
                            nccl_comm, level_by_level or MF_LEAF_CUBLAS      */
-  int32_t comm_regions;   /* sharded plans with nccl_comm (MF_OUT_ROOT / _ALL): the
-                           leaf and post-addition run in this many 128-aligned
-                           row regions, and each region's rows of C are reduced
-                           on a separate stream while the next region computes
-                           ("reduce C block-groups as
-                           products complete").  0 = default (8 when
-                           shard_count > 1, else 1); 1 = one reduce after K6.
-                           Without nccl_comm an explicit value > 1 still runs
+  int32_t comm_regions;   /* sharded plans with comm: the leaf and post-addition
+                           run in this many 128-aligned row regions, and each
+                           region's rows of C are summed on the exchange stream
+                           while the next region computes (SURVEY §8f NEXT-4:
+                           "reduce C block-groups as products complete") --
+                           reduce (MF_OUT_ROOT), all-reduce (MF_OUT_ALL) or a
+                           reduce onto each owning rank (MF_OUT_ROWSLAB, a
+                           region-wise reduce-scatter).  Also the number of
+                           MF_IN_ROOT input slabs.  0 = default (8 when
+                           shard_count > 1, else 1); 1 = one collective after
+                           K6.  Without comm an explicit value > 1 still runs
                            the regions (the shard's partial C; for tests)    */
   int32_t recurse_levels; /* with level_by_level = 1: how many top levels run one
                            at a time (0 = levels - 1, the paper's full
@@ -171,11 +183,12 @@ mf_status mf_dgemm(mf_plan_t plan, double alpha, const double* A, int64_t lda,
  * pinned memory is fastest).  Copies A and B to plan-owned device buffers,
  * runs mf_dgemm, copies C back; returns after C is complete on the host.
  * Single-GPU flattened plans pipeline the copies with the compute by row /
- * column slabs.  Sharded plans with an NCCL communicator and
- * MF_IN_REPLICATED inputs copy only their 1/N row slab of A and B and
- * all-gather the rest over NVLink (every rank must pass the full host A, B);
- * with MF_OUT_ROOT only rank 0 copies C back, with MF_OUT_ROWSLAB each rank
- * its slab. */
+ * column slabs.  Sharded plans with a communicator and MF_IN_REPLICATED
+ * inputs copy only their 1/N row slab of A and B and all-gather the rest over
+ * NVLink (every rank must pass the full host A, B); with MF_IN_ROOT only rank
+ * 0 reads (and must pass) host A and B, and the other ranks (A, B may be NULL)
+ * receive them by the slab broadcasts of mf_dgemm; with MF_OUT_ROOT only rank
+ * 0 copies C back, with MF_OUT_ROWSLAB each rank its slab. */
 mf_status mf_dgemm_host(mf_plan_t plan, double alpha, const double* A, int64_t lda,
                         const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
@@ -220,6 +233,18 @@ mf_status mf_plan_info(mf_plan_t plan, size_t* workspace_bytes, int64_t* leaf_n,
 mf_status mf_plan_products(mf_plan_t plan, int32_t* a_src, int32_t* a_idx, int32_t* b_src,
                            int32_t* b_idx, int32_t* sign, int32_t* shard);
 
+/* Provenance of the plan's pre/post-addition kernels (K4/K6), for tests that
+ * must know which implementation ran: *jit_tables = coefficient tables for
+ * which mf_plan asked NVRTC for a generated kernel, *jit_built = how many it
+ * built and loaded (fewer: NVRTC / driver API missing, or compilation failed;
+ * those tables run the table-driven kernels); launches[4] = K4/K6 launches
+ * since the plan was made by kind: [0] table-driven (mf_mix.cu), [1]
+ * compiled-in specialised (mf_fixed.cu), [2] Kronecker-factored (mf_kron.cu),
+ * [3] generated at plan time.  A level-by-level plan sums its child plans.
+ * Any pointer may be NULL. */
+mf_status mf_plan_kernels(mf_plan_t plan, int32_t* jit_tables, int32_t* jit_built,
+                          int64_t* launches /* 4 */);
+
 /* Product sharding: with shard_count = N, rank r computes
  * floor(R^L / N) whole products (a contiguous range) and, of each of the
  * R^L mod N leftover products (shard[q] = -1), the 128-aligned output row slab
@@ -252,13 +277,38 @@ mf_status mf_postmix(mf_plan_t plan, double alpha, const double* P, double* C, i
  * *calls = number of mf_dgemm calls summed; reset != 0 clears the sums. */
 mf_status mf_profile_read(mf_plan_t plan, double* ms /* 5 */, int32_t* calls, int32_t reset);
 
-/* Multi-GPU bootstrap (NCCL over NVLink; the 128-byte unique id is exchanged
- * by the caller, e.g. through torch.distributed).  Each rank then passes the
- * communicator in mf_options.nccl_comm with shard_rank = rank and
- * shard_count = nranks; mf_dgemm computes the rank's products and sums the
- * partial C with ncclReduce (MF_OUT_ROOT) or ncclAllReduce (MF_OUT_ALL). */
+/* Communicators of the product-sharded path.  The
+ * paper's recursion makes the R^L leaf products independent ("each product can
+ * be done recursively", Eq. "strassen" L196-202) and the
+ * post-addition C_i = sum_q W[i][q] P_q is linear, so rank r computes the
+ * products of shard r and the partial C sums of all ranks add up to C.  Each
+ * rank passes its handle in mf_options.comm with shard_rank = rank and
+ * shard_count = nranks; every rank then calls mf_dgemm (or mf_dgemm_host)
+ * collectively with the same arguments, and the library broadcasts the inputs
+ * (MF_IN_ROOT) and sums the partial C (mf_options.output_mode).
+ *
+ * NCCL (one process per GPU, NVLink / NVSwitch): the 128-byte unique id of
+ * mf_nccl_unique_id is exchanged by the caller (e.g. torch.distributed); the
+ * returned handle owns the ncclComm_t.  libnccl.so.2 is loaded at run time
+ * (MF_ERR_NCCL if absent).
+ *
+ * Loopback (mf_loop_comm_create): nranks handles for ranks that are THREADS of
+ * one process (on one device, or on devices with peer access).  Every
+ * collective is a host rendezvous of the threads followed by stream-ordered
+ * copies and a summation kernel (ascending rank order) that each receiving
+ * rank enqueues on its own stream behind the senders' events; no kernel waits
+ * on another rank's kernel.  It runs the multi-rank schedule where fewer GPUs
+ * than ranks exist (tests).  A rank that stops calling collectives makes its
+ * peers fail with MF_ERR_NCCL after 120 s.  nranks <= 16.
+ *
+ * mf_comm_destroy frees either kind (NULL: no-op); mf_nccl_comm_destroy is the
+ * same call.  Destroy a handle only after the plans using it. */
+enum { MF_COMM_NCCL = 0, MF_COMM_LOOPBACK = 1 };
 mf_status mf_nccl_unique_id(void* id_out /* 128 bytes */);
 mf_status mf_nccl_comm_create(void** comm_out, const void* id, int32_t rank, int32_t nranks);
+mf_status mf_loop_comm_create(int32_t nranks, void** comms_out /* nranks handles */);
+mf_status mf_comm_info(void* comm, int32_t* rank, int32_t* nranks, int32_t* kind);
+mf_status mf_comm_destroy(void* comm);
 mf_status mf_nccl_comm_destroy(void* comm);
 
 /* Diagnostic: generate the fused-addition kernel mf_plan would build at run

@@ -40,13 +40,15 @@ OUT_ROOT, OUT_ALL, OUT_ROWSLAB = 0, 1, 2
 EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error", "mf_plan_info",
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
            "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
-           "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync", "mf_jit_compile_check")
+           "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync", "mf_jit_compile_check",
+           "mf_loop_comm_create", "mf_comm_info", "mf_comm_destroy", "mf_plan_kernels")
+COMM_NCCL, COMM_LOOPBACK = 0, 1
 
 
 class mf_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("leaf", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
-                ("shard_count", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
+                ("shard_count", ctypes.c_int32), ("comm", ctypes.c_void_p),
                 ("input_mode", ctypes.c_int32), ("output_mode", ctypes.c_int32),
                 ("profile", ctypes.c_int32), ("host_only", ctypes.c_int32),
                 ("level_by_level", ctypes.c_int32), ("max_workspace", ctypes.c_int64),
@@ -69,6 +71,7 @@ _lib.mf_plan_info.argtypes = [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTE
                               ctypes.POINTER(_I64), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
 _lib.mf_plan_products.argtypes = [_P] * 7
 _lib.mf_plan_shard_rows.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
+_lib.mf_plan_kernels.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), _P]
 _lib.mf_premix.argtypes = [_P, _I32, _P, _I64, _P, _P]
 _lib.mf_leaf.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _P, _P]
 _lib.mf_postmix.argtypes = [_P, _D, _P, _P, _I64, _P]
@@ -76,6 +79,9 @@ _lib.mf_profile_read.argtypes = [_P, _P, ctypes.POINTER(_I32), _I32]
 _lib.mf_nccl_unique_id.argtypes = [_P]
 _lib.mf_nccl_comm_create.argtypes = [ctypes.POINTER(_P), _P, _I32, _I32]
 _lib.mf_nccl_comm_destroy.argtypes = [_P]
+_lib.mf_loop_comm_create.argtypes = [_I32, ctypes.POINTER(_P)]
+_lib.mf_comm_info.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
+_lib.mf_comm_destroy.argtypes = [_P]
 _lib.mf_jit_compile_check.argtypes = [_P, _I32, _I32, _I32, _I32, ctypes.c_char_p,
                                       ctypes.POINTER(_I32), ctypes.POINTER(_I64)]
 for _f in EXPORTS:
@@ -134,7 +140,8 @@ class Plan:
 
     def __init__(self, triple: triples.Triple | None, levels: int, n: int, *, leaf: str = "dmma",
                  device: int | None = None, shard_rank: int = 0, shard_count: int = 1,
-                 nccl_comm=None, input_mode: int = IN_REPLICATED, output_mode: int = OUT_ROOT,
+                 comm=None, nccl_comm=None, input_mode: int = IN_REPLICATED,
+                 output_mode: int = OUT_ROOT,
                  profile: bool = False, host_only: bool = False, level_by_level: bool = False,
                  max_workspace: int = 0, fuse_postadd: bool = False, recurse_levels: int = 0,
                  graph: bool = False, comm_regions: int = 0):
@@ -144,7 +151,8 @@ class Plan:
         opt.device = -1 if device is None else int(device)
         opt.leaf = {"dmma": LEAF_DMMA, "simple": LEAF_SIMPLE, "cublas": LEAF_CUBLAS}[leaf]
         opt.shard_rank, opt.shard_count = int(shard_rank), int(shard_count)
-        opt.nccl_comm = nccl_comm.value if isinstance(nccl_comm, ctypes.c_void_p) else nccl_comm
+        comm = comm if comm is not None else nccl_comm  # (nccl_comm: the round-1 keyword)
+        opt.comm = comm.value if isinstance(comm, ctypes.c_void_p) else comm
         opt.input_mode, opt.output_mode = int(input_mode), int(output_mode)
         opt.profile = int(bool(profile))
         opt.host_only = int(bool(host_only))
@@ -196,6 +204,17 @@ class Plan:
         out["calls"] = calls.value
         return out
 
+    KERNEL_KINDS = ("table", "fixed", "kron", "jit")
+
+    def kernels(self) -> dict:
+        """mf_plan_kernels: generated-kernel tables requested / built, and K4/K6
+        launches so far by kind (table-driven, compiled-in, Kronecker, generated)."""
+        jt, jb = _I32(), _I32()
+        launches = (ctypes.c_int64 * 4)()
+        _check(_lib.mf_plan_kernels(self._h, ctypes.byref(jt), ctypes.byref(jb), launches))
+        return {"jit_tables": jt.value, "jit_built": jb.value,
+                "launches": dict(zip(self.KERNEL_KINDS, list(launches)))}
+
     def shard_rows(self) -> tuple:
         """Row slab [r0, r1) this rank computes of each split product (0, 0 if none)."""
         r0, r1 = _I64(), _I64()
@@ -221,14 +240,17 @@ class Plan:
     def c_rows(self) -> int:
         """Rows of this rank's C: n, or n / shard_count with MF_OUT_ROWSLAB."""
         o = self._opt
-        if o.output_mode == OUT_ROWSLAB and o.nccl_comm and o.shard_count > 1:
+        if o.output_mode == OUT_ROWSLAB and o.comm and o.shard_count > 1:
             return self.n // o.shard_count
         return self.n
 
-    def dgemm_host(self, A: np.ndarray, B: np.ndarray, C: np.ndarray | None = None,
+    def dgemm_host(self, A: np.ndarray | None, B: np.ndarray | None, C: np.ndarray | None = None,
                    alpha: float = 1.0, stream=None) -> np.ndarray:
-        """The same product on HOST float64 row-major arrays (copies inside the call)."""
+        """The same product on HOST float64 row-major arrays (copies inside the call).
+        With IN_ROOT, ranks other than 0 may pass None for A and B."""
         def host(X, name, rows=self.n):
+            if X is None:
+                return None, self.n
             if X.dtype != np.float64 or X.ndim != 2 or X.shape != (rows, self.n) or \
                     X.strides[1] != 8:
                 raise ValueError(f"{name} must be a row-major {rows}x{self.n} float64 array")
@@ -330,5 +352,25 @@ def nccl_comm_destroy(comm: ctypes.c_void_p):
     _check(_lib.mf_nccl_comm_destroy(comm))
 
 
+def loop_comm_create(nranks: int) -> list:
+    """mf_loop_comm_create: handles for `nranks` ranks run as threads of this
+    process (each thread passes its handle as Plan(comm=...))."""
+    arr = (_P * int(nranks))()
+    _check(_lib.mf_loop_comm_create(int(nranks), arr))
+    return [ctypes.c_void_p(arr[i]) for i in range(int(nranks))]
+
+
+def comm_info(comm) -> dict:
+    r, n, k = _I32(), _I32(), _I32()
+    _check(_lib.mf_comm_info(comm, ctypes.byref(r), ctypes.byref(n), ctypes.byref(k)))
+    return {"rank": r.value, "nranks": n.value,
+            "kind": {COMM_NCCL: "nccl", COMM_LOOPBACK: "loopback"}[k.value]}
+
+
+def comm_destroy(comm):
+    _check(_lib.mf_comm_destroy(comm))
+
+
 __all__ = ["Plan", "dgemm", "MfError", "triples", "version", "nccl_unique_id", "nccl_comm_create",
-           "nccl_comm_destroy", "EXPORTS", "LIB_PATH"]
+           "nccl_comm_destroy", "loop_comm_create", "comm_info", "comm_destroy", "EXPORTS",
+           "LIB_PATH"]

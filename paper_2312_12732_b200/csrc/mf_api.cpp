@@ -3,7 +3,6 @@
 // host-buffer entry point and the NCCL bootstrap.  Kernels live in
 // mf_mix.cu (K4/K6) and mf_leaf.cu (K5).
 #include <dlfcn.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -21,7 +20,7 @@ using namespace mf;
 
 struct mf_plan_st : public Plan {};
 
-namespace {
+namespace mf {
 
 thread_local std::string g_err;
 
@@ -34,6 +33,10 @@ mf_status fail(mf_status st, const char* fmt, ...) {
   g_err = buf;
   return st;
 }
+
+}  // namespace mf
+
+namespace {
 
 mf_status cuda_fail(cudaError_t e, const char* what) {
   return fail(MF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
@@ -57,54 +60,6 @@ struct DeviceGuard {
     if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
 };
-
-// ---------------------------------------------------------------- NCCL (dlopen)
-struct Nccl {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
-                         cudaStream_t) = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
-                                ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-
-Nccl* nccl() {
-  static Nccl n;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    // Prefer the NCCL already loaded into the process (torch's), else the loader path.
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
-    n.h = h;
-    n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
-    n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
-    n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
-    n.Reduce = (decltype(n.Reduce))dlsym(h, "ncclReduce");
-    n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
-    n.Broadcast = (decltype(n.Broadcast))dlsym(h, "ncclBroadcast");
-    n.ReduceScatter = (decltype(n.ReduceScatter))dlsym(h, "ncclReduceScatter");
-    n.AllGather = (decltype(n.AllGather))dlsym(h, "ncclAllGather");
-    n.GroupStart = (decltype(n.GroupStart))dlsym(h, "ncclGroupStart");
-    n.GroupEnd = (decltype(n.GroupEnd))dlsym(h, "ncclGroupEnd");
-    n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
-  });
-  return n.h && n.GetUniqueId && n.CommInitRank && n.Reduce && n.AllReduce && n.Broadcast &&
-                 n.ReduceScatter
-             ? &n
-             : nullptr;
-}
 
 // ------------------------------------------------- cuBLAS (dlopen; MF_LEAF_CUBLAS)
 // The leaf ablation only: the library DGEMM on the same K4/K6 pipeline.
@@ -131,10 +86,6 @@ Cublas* cublas() {
     c.DgemmBatched = (decltype(c.DgemmBatched))dlsym(h, "cublasDgemmBatched");
   });
   return c.h && c.Create && c.Destroy && c.SetStream && c.DgemmBatched ? &c : nullptr;
-}
-
-mf_status nccl_fail(Nccl* n, ncclResult_t r, const char* what) {
-  return fail(MF_ERR_NCCL, "%s: %s", what, n && n->GetErrorString ? n->GetErrorString(r) : "?");
 }
 
 // ---------------------------------------------------------------- triple algebra
@@ -354,6 +305,7 @@ void free_plan(Plan* pl) {
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
                   (void*)pl->split_ws, (void*)pl->split_cnt, (void*)pl->d_tinyU, (void*)pl->d_tinyV,
+                  (void*)pl->rA, (void*)pl->rB,
                   (void*)pl->d_tinyW, (void*)pl->hA2, (void*)pl->hB2,
                   (void*)pl->hC2,
                   (void*)pl->hC})
@@ -365,6 +317,7 @@ void free_plan(Plan* pl) {
     for (cudaEvent_t e : set) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->pipe_events) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->comm_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : pl->in_events) cudaEventDestroy(e);
   for (cudaEvent_t e : {pl->set_free[0], pl->set_free[1], pl->compute_done, pl->ser_in[0],
                         pl->ser_in[1], pl->ser_done[0], pl->ser_done[1]})
     if (e) cudaEventDestroy(e);
@@ -374,7 +327,7 @@ void free_plan(Plan* pl) {
     for (MixTable* t : {&b.mixA, &b.mixB, &b.mixC}) jit_free(*t);
   }
   for (MixTable* t : {&pl->mixA, &pl->mixB, &pl->mixC, &pl->mixA2, &pl->mixC2}) jit_free(*t);
-  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm, pl->cs1})
+  for (cudaStream_t st : {pl->h2d, pl->d2h, pl->mixs, pl->s2, pl->comm_s, pl->cs1})
     if (st) cudaStreamDestroy(st);
 }
 
@@ -563,6 +516,17 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   const int shard_count = o.shard_count > 1 ? o.shard_count : 1;
   if (o.shard_rank < 0 || o.shard_rank >= shard_count)
     return fail(MF_ERR_INVALID_ARG, "shard_rank %d outside [0, %d)", o.shard_rank, shard_count);
+  if (o.comm) {
+    // the communicator fixes the sharding: rank r of N computes shard r of N
+    const Comm* xc = comm_from(o.comm);
+    if (!xc)
+      return fail(MF_ERR_INVALID_ARG,
+                  "mf_options.comm is not a handle from mf_nccl_comm_create / mf_loop_comm_create");
+    if (xc->size != shard_count || xc->rank != o.shard_rank)
+      return fail(MF_ERR_INVALID_ARG,
+                  "shard_rank / shard_count (%d / %d) differ from the communicator's rank / size (%d / %d)",
+                  o.shard_rank, shard_count, xc->rank, xc->size);
+  }
 
   if (levels > 0) {
     mf_status st = brent_check(p, R, U, V, W);
@@ -588,7 +552,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     sub.graph = 0;
     sub.level_by_level = r > 1 ? 1 : 0;
     sub.recurse_levels = r > 1 ? r - 1 : 0;
-    sub.shard_rank = 0; sub.shard_count = 1; sub.nccl_comm = nullptr; sub.profile = 0;
+    sub.shard_rank = 0; sub.shard_count = 1; sub.comm = nullptr; sub.profile = 0;
     sub.input_mode = MF_IN_REPLICATED;
     mf_plan_t parent = nullptr, child = nullptr;
     mf_status st = mf_plan_impl(&parent, p, R, U, V, W, 1, n, &top, false);
@@ -623,7 +587,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   pl->P = (int)P; pl->RL = RL; pl->m = n / P;
   pl->opt = o; pl->leaf = o.leaf; pl->fuse = o.fuse_postadd != 0;
   pl->shard_rank = o.shard_rank; pl->shard_count = shard_count;
-  pl->nccl_comm = o.nccl_comm;
+  pl->comm = comm_from(o.comm);
 
   // ---- flatten: U^(x)L etc. (a5 of SURVEY.md §8a executed as one level) ----
   if (levels == 0) {
@@ -840,7 +804,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       jj.push_back({&b.mixB, pl->P, 0});
       jj.push_back({&b.mixC, 0, pl->P});
     }
-    jit_build_all(jj);
+    for (const JitJob& j : jj) pl->jit_tables += j.t->nout > 0 && jit_shape(*j.t).vw > 0;
+    pl->jit_built = jit_build_all(jj);
   }
   std::vector<LeafJob> jobs;
   std::vector<int32_t> job_q = pl->my_prods;
@@ -948,6 +913,22 @@ mf_status mf_plan_info(mf_plan_t pl, size_t* ws, int64_t* leaf_n, int64_t* n_pro
   return MF_OK;
 }
 
+mf_status mf_plan_kernels(mf_plan_t pl, int32_t* jit_tables, int32_t* jit_built, int64_t* launches) {
+  if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
+  int32_t jt = 0, jb = 0;
+  int64_t l[4] = {0, 0, 0, 0};
+  for (const Plan* q = pl; q; q = q->child) {
+    jt += q->jit_tables;
+    jb += q->jit_built;
+    for (int i = 0; i < 4; ++i) l[i] += q->mix_launches[i];
+  }
+  if (jit_tables) *jit_tables = jt;
+  if (jit_built) *jit_built = jb;
+  if (launches)
+    for (int i = 0; i < 4; ++i) launches[i] = l[i];
+  return MF_OK;
+}
+
 mf_status mf_plan_shard_rows(mf_plan_t pl, int64_t* r0, int64_t* r1) {
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
   if (r0) *r0 = pl->my_part.empty() ? 0 : pl->part_r0;
@@ -982,14 +963,14 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
 static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n);
 
 // Row regions of the region-overlapped exchange (mf_options.comm_regions).
-// Without nccl_comm only an explicit comm_regions > 1 applies (the regions
+// Without a communicator only an explicit comm_regions > 1 applies (the regions
 // are computed, nothing is reduced: the emulated ranks' partial C, for tests).
 static int comm_regions(const Plan& pl) {
-  if ((pl.nccl_comm && pl.opt.output_mode == MF_OUT_ROWSLAB) || pl.child || pl.fuse ||
-      !pl.batches.empty() || pl.levels == 0 || (!pl.nccl_comm && pl.opt.comm_regions <= 1))
+  if (pl.child || pl.fuse || !pl.batches.empty() || pl.levels == 0 ||
+      (!pl.comm && pl.opt.comm_regions <= 1))
     return 1;
   const int want = pl.opt.comm_regions > 0 ? pl.opt.comm_regions
-                                           : (pl.nccl_comm && pl.shard_count > 1 ? 8 : 1);
+                                           : (pl.comm && pl.shard_count > 1 ? 8 : 1);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (pl.m + 127) / 128));
 }
 
@@ -999,7 +980,7 @@ static int comm_regions(const Plan& pl) {
 mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, const double* B,
                    int64_t ldb, double* C, int64_t ldc, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!pl || !pl->opt.graph || pl->opt.profile || pl->opt.host_only || pl->nccl_comm || pl->child ||
+  if (!pl || !pl->opt.graph || pl->opt.profile || pl->opt.host_only || pl->comm || pl->child ||
       pl->leaf == MF_LEAF_CUBLAS || s == nullptr || s == cudaStreamLegacy || s == cudaStreamPerThread)
     return dgemm_eager(pl, alpha, A, lda, B, ldb, C, ldc, stream);
   Plan::GraphKey key;
@@ -1037,13 +1018,30 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
   return MF_OK;
 }
 
+static mf_status ensure_events(std::vector<cudaEvent_t>& v, size_t k) {
+  while (v.size() < k) {
+    cudaEvent_t e;
+    MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    v.push_back(e);
+  }
+  return MF_OK;
+}
+
+// Input row slabs of the MF_IN_ROOT broadcast (and of the K4 launches that
+// follow each slab): as many as the exchange regions, at least 1.
+static int input_slabs(const Plan& pl) {
+  const int want = pl.opt.comm_regions > 0 ? pl.opt.comm_regions : 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (pl.m + 127) / 128));
+}
+
 static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_t lda,
                              const double* B, int64_t ldb, double* C, int64_t ldc, void* stream) {
   g_err.clear();
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   const int64_t n = pl->n;
-  const bool root_inputs = pl->nccl_comm && pl->opt.input_mode == MF_IN_ROOT;
+  Comm* const xc = pl->comm;
+  const bool root_inputs = xc && pl->opt.input_mode == MF_IN_ROOT;
   const bool is_root = pl->shard_rank == 0;
   mf_status st;
   if (!root_inputs || is_root) {
@@ -1051,36 +1049,74 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
       return st;
   }
   // MF_OUT_ROWSLAB: C is this rank's n/N x n row slab of the reduced product
-  const bool rowslab = pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB;
+  const bool rowslab = xc && pl->opt.output_mode == MF_OUT_ROWSLAB;
   const int64_t c_rows = rowslab ? n / pl->shard_count : n;
   if ((st = check_mat("C", C, ldc, n)) != MF_OK) return st;
   if ((A && overlaps(A, lda, n, C, ldc, c_rows, n)) || (B && overlaps(B, ldb, n, C, ldc, c_rows, n)))
     return fail(MF_ERR_INVALID_ARG, "C overlaps A or B");
-  if (rowslab && ldc != n) return fail(MF_ERR_UNSUPPORTED, "MF_OUT_ROWSLAB needs ldc == n");
+  if (xc && ldc != n)
+    return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n (got %lld)", (long long)ldc);
   DeviceGuard guard(pl->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t m = pl->m;
+  if (xc && !pl->comm_s) MF_CUDA(cudaStreamCreateWithFlags(&pl->comm_s, cudaStreamNonBlocking), "stream");
 
-  Nccl* nc = nullptr;
-  if (pl->nccl_comm) {
-    nc = nccl();
-    if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
-  }
+  // a6, input side (MF_IN_ROOT): rank 0's A and B reach the other ranks as
+  // broadcasts of row slabs on the exchange stream -- slab k = rows
+  // [r0_k, r1_k) of every block row, one contiguous piece per block row -- and
+  // each rank's K4 of slab k starts as soon as that slab landed, so K4(A) runs
+  // under the broadcast of B.  Rank 0 sends straight from
+  // its A and B when they are contiguous (ld == n) and computes without waiting.
+  const int KI = root_inputs ? input_slabs(*pl) : 1;
+  bool wait_inputs = false;  // this rank's K4 / leaf wait for the slabs
   if (root_inputs) {
-    // Broadcast rank 0's A and B into plan-owned replicas (contiguous, ld n).
     const size_t bytes = sizeof(double) * n * n;
-    if (!pl->hA && cudaMalloc(&pl->hA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica A");
-    if (!pl->hB && cudaMalloc(&pl->hB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica B");
+    double* bufA = nullptr;
+    double* bufB = nullptr;
     if (is_root) {
-      MF_CUDA(cudaMemcpy2DAsync(pl->hA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy A");
-      MF_CUDA(cudaMemcpy2DAsync(pl->hB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy B");
+      bufA = const_cast<double*>(A);
+      bufB = const_cast<double*>(B);
+      if (lda != n) {
+        if (!pl->rA && cudaMalloc(&pl->rA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica A");
+        MF_CUDA(cudaMemcpy2DAsync(pl->rA, n * 8, A, lda * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "pack A");
+        bufA = pl->rA;
+      }
+      if (ldb != n) {
+        if (!pl->rB && cudaMalloc(&pl->rB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica B");
+        MF_CUDA(cudaMemcpy2DAsync(pl->rB, n * 8, B, ldb * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "pack B");
+        bufB = pl->rB;
+      }
+    } else {
+      if (pl->recvA) bufA = pl->recvA;
+      else if (!pl->rA && cudaMalloc(&pl->rA, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica A");
+      if (pl->recvB) bufB = pl->recvB;
+      else if (!pl->rB && cudaMalloc(&pl->rB, bytes) != cudaSuccess) return fail(MF_ERR_OUT_OF_MEMORY, "replica B");
+      if (!bufA) bufA = pl->rA;
+      if (!bufB) bufB = pl->rB;
+      wait_inputs = true;
     }
-    ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
-    ncclResult_t r;
-    if ((r = nc->Broadcast(pl->hA, pl->hA, (size_t)n * n, ncclDouble, 0, comm, s)) != ncclSuccess)
-      return nccl_fail(nc, r, "ncclBroadcast(A)");
-    if ((r = nc->Broadcast(pl->hB, pl->hB, (size_t)n * n, ncclDouble, 0, comm, s)) != ncclSuccess)
-      return nccl_fail(nc, r, "ncclBroadcast(B)");
-    A = pl->hA; lda = n; B = pl->hB; ldb = n;
+    if ((st = ensure_events(pl->in_events, 2 * (size_t)KI + 2)) != MF_OK) return st;
+    // the exchange stream starts after the caller's prior work (packing, and
+    // the previous call's reads of the replicas)
+    MF_CUDA(cudaEventRecord(pl->in_events[2 * KI + 1], s), "event");
+    MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->in_events[2 * KI + 1], 0), "wait");
+    for (int side = 0; side < 2; ++side) {
+      double* buf = side == 0 ? bufA : bufB;
+      for (int k = 0; k < KI; ++k) {
+        const auto sr = tile_piece(m, k, KI);
+        if ((st = xc->group_start()) != MF_OK) return st;
+        for (int br = 0; br < pl->P && sr.second > sr.first; ++br)
+          if ((st = xc->bcast(buf + (br * m + sr.first) * n, (size_t)(sr.second - sr.first) * n, 0,
+                              pl->comm_s)) != MF_OK) {
+            xc->group_end();
+            return st;
+          }
+        if ((st = xc->group_end()) != MF_OK) return st;
+        MF_CUDA(cudaEventRecord(pl->in_events[side * KI + k], pl->comm_s), "event");
+      }
+    }
+    MF_CUDA(cudaEventRecord(pl->in_events[2 * KI], pl->comm_s), "event");  // all landed
+    A = bufA; lda = n; B = bufB; ldb = n;
   }
 
   double* const C_out = C;
@@ -1094,6 +1130,34 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
   if (pl->opt.profile) ++pl->prof_calls;
   bool reduced = false;  // C already summed over ranks region by region
   auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
+  // K4 of one side for this shard (whole products' slots, then the split
+  // products' slots on the rank's row slab), slab by slab behind the input
+  // broadcast when this rank receives its inputs
+  auto premix_side = [&](int side) -> mf_status {
+    const MixTable& whole = side == 0 ? pl->mixA : pl->mixB;
+    const double* X = side == 0 ? A : B;
+    const int64_t ldx = side == 0 ? lda : ldb;
+    double* out = side == 0 ? pl->T : pl->S;
+    const int nk = wait_inputs ? KI : 1;
+    for (int k = 0; k < nk; ++k) {
+      Rows r;
+      if (wait_inputs) {
+        MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[side * KI + k], 0), "wait");
+        const auto sr = tile_piece(m, k, KI);
+        r.r0 = sr.first; r.r1 = sr.second;
+        if (r.r1 <= r.r0) continue;
+      }
+      MF_CUDA(launch_premix(*pl, whole, X, ldx, out, s, r), side == 0 ? "pre-add A (K4)" : "pre-add B (K4)");
+      if (side == 0 && !pl->my_part.empty()) {
+        Rows pr;
+        pr.r0 = std::max<int64_t>(r.r0, pl->part_r0);
+        pr.r1 = std::min<int64_t>(r.end(m), pl->part_r1);
+        if (pr.r0 < pr.r1)
+          MF_CUDA(launch_premix(*pl, pl->mixA2, X, ldx, out, s, pr), "pre-add A (K4, split)");
+      }
+    }
+    return MF_OK;
+  };
   mark(0);
   if (tiny_eligible(*pl) && !getenv("MF_TINY_OFF")) {
     // n <= 64: the whole level in one cluster launch (profile: the leaf phase)
@@ -1102,6 +1166,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     mark(3);
   } else if (pl->levels == 0) {
     mark(1); mark(2);
+    if (wait_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
     if ((st = run_leaf(*pl, A, lda, B, ldb, nullptr, nullptr, C, ldc, 0, alpha, s)) != MF_OK) return st;
     mark(3);
   } else if (!pl->batches.empty()) {
@@ -1129,15 +1194,11 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     // adds alpha * W'[i][q] * P_q into each C block i (no K6, no P workspace)
     // (profile: the memset is timed with pre-add A)
     MF_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, n * 8, n, s), "zero C");
-    MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
-    if (!pl->my_part.empty()) {
-      Rows pr;
-      pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
-      MF_CUDA(launch_premix(*pl, pl->mixA2, A, lda, pl->T, s, pr), "pre-add A (K4, split)");
-    }
+    if ((st = premix_side(0)) != MF_OK) return st;
     mark(1);
-    MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
+    if ((st = premix_side(1)) != MF_OK) return st;
     mark(2);
+    if (wait_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
     if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, C, ldc, 0, alpha, s)) != MF_OK) return st;
     if (!pl->my_part.empty()) {
       Rows pr;
@@ -1148,19 +1209,16 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     mark(3);
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
-    MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s), "pre-add A (K4)");
-    if (!pl->my_part.empty()) {
-      Rows pr;
-      pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
-      MF_CUDA(launch_premix(*pl, pl->mixA2, A, lda, pl->T, s, pr), "pre-add A (K4, split)");
-    }
+    if ((st = premix_side(0)) != MF_OK) return st;
     mark(1);
-    MF_CUDA(launch_premix(*pl, pl->mixB, B, ldb, pl->S, s), "pre-add B (K4)");
+    if ((st = premix_side(1)) != MF_OK) return st;
     mark(2);
+    // aliased operands are read by the leaf straight from the received inputs
+    if (wait_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
     if (pl->child) {
       // a5: level by level -- each product P_q' = X_q Y_q is itself computed by
       // the (levels-1)-level child plan ("recursively solve P_i")
-      const int64_t m = pl->m, mm = m * m;
+      const int64_t mm = m * m;
       for (int32_t q : pl->my_prods) {
         const Product& pr = pl->prods[q];
         const double* X = pr.a_src == SRC_WORKSPACE
@@ -1178,19 +1236,15 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     } else if (comm_regions(*pl) > 1) {
       // a3 + a4 + a6 by row regions (NEXT-4): region k's leaf products and
       // post-addition, then its rows of the partial C (one contiguous piece per
-      // block row) are reduced on pl->comm while region k+1 computes.  Every
-      // rank issues the same collectives in the same order.
+      // block row) are summed on the exchange stream while region k+1
+      // computes -- reduced onto rank 0 (MF_OUT_ROOT), onto every rank
+      // (MF_OUT_ALL), or onto the rank whose output row slab holds them
+      // (MF_OUT_ROWSLAB: a region-wise reduce-scatter).  Every rank issues the
+      // same collectives in the same order.
       const int K = comm_regions(*pl);
-      if (pl->nccl_comm && ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");
-      if (!pl->comm) MF_CUDA(cudaStreamCreateWithFlags(&pl->comm, cudaStreamNonBlocking), "stream");
-      while ((int)pl->comm_events.size() < K + 1) {
-        cudaEvent_t e;
-        MF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-        pl->comm_events.push_back(e);
-      }
-      ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
-      const bool exchange = comm != nullptr;
-      const int64_t m = pl->m;
+      if (!pl->comm_s) MF_CUDA(cudaStreamCreateWithFlags(&pl->comm_s, cudaStreamNonBlocking), "stream");
+      if ((st = ensure_events(pl->comm_events, (size_t)K + 1)) != MF_OK) return st;
+      const bool exchange = xc != nullptr;
       auto post = [&](int64_t a, int64_t b, const MixTable& t) -> mf_status {
         if (a >= b) return MF_OK;
         Rows q;
@@ -1199,7 +1253,8 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
         return MF_OK;
       };
       MF_CUDA(cudaEventRecord(pl->comm_events[K], s), "event");
-      MF_CUDA(cudaStreamWaitEvent(pl->comm, pl->comm_events[K], 0), "wait");  // comm after K4
+      MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->comm_events[K], 0), "wait");  // exchange after K4
+      const int64_t slab = n / pl->shard_count;  // MF_OUT_ROWSLAB rows per rank
       for (int k = 0; k < K; ++k) {
         const auto rg = tile_piece(m, k, K);
         if (rg.second <= rg.first) continue;
@@ -1224,35 +1279,42 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
         }
         if (!exchange) continue;
         MF_CUDA(cudaEventRecord(pl->comm_events[k], s), "event");
-        MF_CUDA(cudaStreamWaitEvent(pl->comm, pl->comm_events[k], 0), "wait");
-        const size_t count = (size_t)(rg.second - rg.first) * n;
-        nc->GroupStart();
+        MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->comm_events[k], 0), "wait");
+        if ((st = xc->group_start()) != MF_OK) return st;
         for (int br = 0; br < pl->P; ++br) {
-          double* piece = C + (br * m + rg.first) * n;
-          ncclResult_t rr = pl->opt.output_mode == MF_OUT_ALL
-                                ? nc->AllReduce(piece, piece, count, ncclDouble, ncclSum, comm, pl->comm)
-                                : nc->Reduce(piece, piece, count, ncclDouble, ncclSum, 0, comm, pl->comm);
-          if (rr != ncclSuccess) {
-            nc->GroupEnd();
-            return nccl_fail(nc, rr, "ncclReduce(C region)");
+          const int64_t row0 = br * m + rg.first, row1 = br * m + rg.second;
+          double* piece = C + row0 * n;
+          if (rowslab) {
+            // the rows of this piece owned by each rank's output slab
+            for (int64_t o = row0 / slab; o * slab < row1; ++o) {
+              const int64_t a = std::max<int64_t>(row0, o * slab), b = std::min<int64_t>(row1, (o + 1) * slab);
+              double* recv = o == pl->shard_rank ? C_out + (a - o * slab) * n : C + a * n;
+              st = xc->reduce(C + a * n, recv, (size_t)(b - a) * n, (int)o, pl->comm_s);
+              if (st != MF_OK) break;
+            }
+          } else {
+            const size_t count = (size_t)(row1 - row0) * n;
+            st = pl->opt.output_mode == MF_OUT_ALL ? xc->allreduce(piece, piece, count, pl->comm_s)
+                                                   : xc->reduce(piece, piece, count, 0, pl->comm_s);
+          }
+          if (st != MF_OK) {
+            xc->group_end();
+            return st;
           }
         }
-        ncclResult_t rr = nc->GroupEnd();
-        if (rr != ncclSuccess) return nccl_fail(nc, rr, "ncclGroupEnd");
+        if ((st = xc->group_end()) != MF_OK) return st;
       }
-      MF_CUDA(cudaEventRecord(pl->comm_events[K], pl->comm), "event");
+      MF_CUDA(cudaEventRecord(pl->comm_events[K], pl->comm_s), "event");
       MF_CUDA(cudaStreamWaitEvent(s, pl->comm_events[K], 0), "wait");
       reduced = true;  // (without a communicator: the region K6 wrote the partial C)
     } else {
       // a3: all leaf products in one launch (K5); split products on this rank's slab
-      if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s)) !=
-          MF_OK)
+      if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s)) != MF_OK)
         return st;
       if (!pl->my_part.empty()) {
         Rows pr;
         pr.r0 = pl->part_r0; pr.r1 = pl->part_r1;
-        if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, pl->m, pl->m * pl->m, 1.0, s, pr,
-                           true)) != MF_OK)
+        if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, pr, true)) != MF_OK)
           return st;
       }
     }
@@ -1273,17 +1335,16 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     }
   }
   mark(4);
-  if (pl->nccl_comm && !reduced) {
+  if (xc && !reduced) {
     // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
-    ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
-    if (ldc != n) return fail(MF_ERR_UNSUPPORTED, "multi-GPU reduction needs ldc == n");
-    ncclResult_t r =
-        rowslab ? nc->ReduceScatter(C, C_out, (size_t)c_rows * n, ncclDouble, ncclSum, comm, s)
-        : pl->opt.output_mode == MF_OUT_ALL
-            ? nc->AllReduce(C, C, (size_t)n * n, ncclDouble, ncclSum, comm, s)
-            : nc->Reduce(C, C, (size_t)n * n, ncclDouble, ncclSum, 0, comm, s);
-    if (r != ncclSuccess) return nccl_fail(nc, r, "ncclReduce(C)");
+    st = rowslab ? xc->reduce_scatter(C, C_out, (size_t)c_rows * n, s)
+         : pl->opt.output_mode == MF_OUT_ALL ? xc->allreduce(C, C, (size_t)n * n, s)
+                                             : xc->reduce(C, C, (size_t)n * n, 0, s);
+    if (st != MF_OK) return st;
   }
+  // the call's stream ends after the input broadcast (rank 0 sends from the
+  // caller's A and B, which must stay untouched until then)
+  if (root_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
   mark(5);
   return MF_OK;
 }
@@ -1325,7 +1386,7 @@ mf_status mf_profile_read(mf_plan_t pl, double* ms, int32_t* calls, int32_t rese
 // per element) unless mf_dgemm's leaf cut a few-wave launch's tail into
 // split-K pieces (region launches never split); then they agree to rounding.
 static int pipeline_slabs(const Plan& pl) {
-  if (pl.nccl_comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
+  if (pl.comm || pl.shard_count > 1 || pl.leaf != MF_LEAF_DMMA || pl.child ||
       !pl.batches.empty() || pl.fuse)
     return 1;
   // as many slabs as keep every region launch above 1.3 waves of 128x128
@@ -1393,9 +1454,13 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
   if (pl->opt.host_only) return fail(MF_ERR_INVALID_ARG, "host-only plan cannot compute");
   const int64_t n = pl->n;
   mf_status st;
-  if ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK ||
-      (st = check_mat("C", C, ldc, n)) != MF_OK)
+  // MF_IN_ROOT: only rank 0's host A and B are read (the others may pass NULL)
+  const bool root_in = pl->comm && pl->opt.input_mode == MF_IN_ROOT;
+  const bool reads_inputs = !root_in || pl->shard_rank == 0;
+  if (reads_inputs &&
+      ((st = check_mat("A", A, lda, n)) != MF_OK || (st = check_mat("B", B, ldb, n)) != MF_OK))
     return st;
+  if ((st = check_mat("C", C, ldc, n)) != MF_OK) return st;
   DeviceGuard guard(pl->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t bytes = sizeof(double) * n * n;
@@ -1428,48 +1493,56 @@ static mf_status host_call(mf_plan_t pl, double alpha, const double* A, int64_t 
     // a set is refilled once its previous call's copy out (after its compute) is done
     if (async && pl->set_busy[set]) MF_CUDA(cudaStreamWaitEvent(cin, pl->set_free[set], 0), "wait");
     const int N = pl->shard_count;
-    Nccl* nc = pl->nccl_comm ? nccl() : nullptr;
-    const bool slabs = nc && nc->AllGather && n % N == 0 && pl->opt.input_mode == MF_IN_REPLICATED &&
+    Comm* const xc = pl->comm;
+    const bool slabs = xc && n % N == 0 && pl->opt.input_mode == MF_IN_REPLICATED &&
                        !getenv("MF_HOST_FULLCOPY");
     const int64_t rows = slabs ? n / N : n, r0 = slabs ? (int64_t)pl->shard_rank * rows : 0;
     // product-sharded ranks with replicated host inputs copy only their 1/N
-    // row slab of A and B over their own PCIe link; NCCL all-gathers the rest
-    // over NVLink (in place) -- host traffic per GPU falls by N
-    MF_CUDA(cudaMemcpy2DAsync(dA + r0 * n, n * 8, A + r0 * lda, lda * 8, n * 8, rows,
-                              cudaMemcpyHostToDevice, cin), "H2D A");
-    MF_CUDA(cudaMemcpy2DAsync(dB + r0 * n, n * 8, B + r0 * ldb, ldb * 8, n * 8, rows,
-                              cudaMemcpyHostToDevice, cin), "H2D B");
+    // row slab of A and B over their own PCIe link; the exchange all-gathers
+    // the rest over NVLink (in place) -- host traffic per GPU falls by N.
+    // MF_IN_ROOT: rank 0 alone copies A and B in; mf_dgemm broadcasts them
+    // into the other ranks' device sets (slab by slab, under their K4).
+    if (reads_inputs) {
+      MF_CUDA(cudaMemcpy2DAsync(dA + r0 * n, n * 8, A + r0 * lda, lda * 8, n * 8, rows,
+                                cudaMemcpyHostToDevice, cin), "H2D A");
+      MF_CUDA(cudaMemcpy2DAsync(dB + r0 * n, n * 8, B + r0 * ldb, ldb * 8, n * 8, rows,
+                                cudaMemcpyHostToDevice, cin), "H2D B");
+    }
     if (async) {
       MF_CUDA(cudaEventRecord(pl->ser_in[set], cin), "event");
       MF_CUDA(cudaStreamWaitEvent(cc, pl->ser_in[set], 0), "wait");
     }
     if (slabs) {
-      ncclComm_t comm = static_cast<ncclComm_t>(pl->nccl_comm);
-      ncclResult_t r;
-      if ((r = nc->GroupStart()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupStart");
-      if ((r = nc->AllGather(dA + r0 * n, dA, (size_t)rows * n, ncclDouble, comm, cc)) != ncclSuccess) {
-        nc->GroupEnd();
-        return nccl_fail(nc, r, "ncclAllGather(A)");
+      if ((st = xc->group_start()) != MF_OK) return st;
+      if ((st = xc->allgather(dA + r0 * n, dA, (size_t)rows * n, cc)) != MF_OK ||
+          (st = xc->allgather(dB + r0 * n, dB, (size_t)rows * n, cc)) != MF_OK) {
+        xc->group_end();
+        return st;
       }
-      if ((r = nc->AllGather(dB + r0 * n, dB, (size_t)rows * n, ncclDouble, comm, cc)) != ncclSuccess) {
-        nc->GroupEnd();
-        return nccl_fail(nc, r, "ncclAllGather(B)");
-      }
-      if ((r = nc->GroupEnd()) != ncclSuccess) return nccl_fail(nc, r, "ncclGroupEnd");
+      if ((st = xc->group_end()) != MF_OK) return st;
     }
-    mf_options saved = pl->opt;
-    pl->opt.input_mode = MF_IN_REPLICATED;
-    st = mf_dgemm(pl, alpha, dA, n, dB, n, dC, n, cc);
-    pl->opt = saved;
+    if (root_in && !reads_inputs) {
+      pl->recvA = dA;  // receive rank 0's broadcast into this device set
+      pl->recvB = dB;
+      st = mf_dgemm(pl, alpha, nullptr, n, nullptr, n, dC, n, cc);
+      pl->recvA = pl->recvB = nullptr;
+    } else if (slabs) {
+      mf_options saved = pl->opt;  // inputs are replicated now
+      pl->opt.input_mode = MF_IN_REPLICATED;
+      st = mf_dgemm(pl, alpha, dA, n, dB, n, dC, n, cc);
+      pl->opt = saved;
+    } else {
+      st = mf_dgemm(pl, alpha, dA, n, dB, n, dC, n, cc);
+    }
     if (st != MF_OK) return st;
     if (async) {
       MF_CUDA(cudaEventRecord(pl->ser_done[set], cc), "event");
       MF_CUDA(cudaStreamWaitEvent(cout, pl->ser_done[set], 0), "wait");
     }
     const int64_t c_rows =
-        pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROWSLAB ? n / pl->shard_count : n;
+        pl->comm && pl->opt.output_mode == MF_OUT_ROWSLAB ? n / pl->shard_count : n;
     // MF_OUT_ROOT: C is defined on rank 0 only -- the other ranks copy nothing back
-    const bool want_c = !(pl->nccl_comm && pl->opt.output_mode == MF_OUT_ROOT && pl->shard_rank != 0);
+    const bool want_c = !(pl->comm && pl->opt.output_mode == MF_OUT_ROOT && pl->shard_rank != 0);
     if (want_c)
       MF_CUDA(cudaMemcpy2DAsync(C, ldc * 8, dC, n * 8, n * 8, c_rows, cudaMemcpyDeviceToHost, cout), "D2H C");
     if (async) {
@@ -1697,42 +1770,6 @@ mf_status mf_postmix(mf_plan_t pl, double alpha, const double* P, double* C, int
   DeviceGuard guard(pl->device);
   MF_CUDA(launch_postmix(*pl, pl->mixC, alpha, P, C, ldc, static_cast<cudaStream_t>(stream)),
           "post-add (K6)");
-  return MF_OK;
-}
-
-mf_status mf_nccl_unique_id(void* id_out) {
-  g_err.clear();
-  Nccl* nc = nccl();
-  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
-  if (!id_out) return fail(MF_ERR_INVALID_ARG, "id_out is NULL");
-  ncclUniqueId id;
-  ncclResult_t r = nc->GetUniqueId(&id);
-  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclGetUniqueId");
-  memcpy(id_out, &id, sizeof id);
-  return MF_OK;
-}
-
-mf_status mf_nccl_comm_create(void** comm_out, const void* id, int32_t rank, int32_t nranks) {
-  g_err.clear();
-  Nccl* nc = nccl();
-  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
-  if (!comm_out || !id || rank < 0 || rank >= nranks) return fail(MF_ERR_INVALID_ARG, "bad argument");
-  ncclUniqueId uid;
-  memcpy(&uid, id, sizeof uid);
-  ncclComm_t comm;
-  ncclResult_t r = nc->CommInitRank(&comm, nranks, uid, rank);
-  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclCommInitRank");
-  *comm_out = comm;
-  return MF_OK;
-}
-
-mf_status mf_nccl_comm_destroy(void* comm) {
-  g_err.clear();
-  if (!comm) return MF_OK;
-  Nccl* nc = nccl();
-  if (!nc) return fail(MF_ERR_NCCL, "libnccl.so.2 could not be loaded");
-  ncclResult_t r = nc->CommDestroy(static_cast<ncclComm_t>(comm));
-  if (r != ncclSuccess) return nccl_fail(nc, r, "ncclCommDestroy");
   return MF_OK;
 }
 

@@ -13,6 +13,36 @@
 
 namespace mf {
 
+// error reporting (mf_api.cpp): sets the thread-local message of mf_last_error
+mf_status fail(mf_status st, const char* fmt, ...);
+
+// The exchange layer of the sharded path (mf_comm.cu): NCCL across processes,
+// or N in-process loopback ranks (threads).  Handles returned through the ABI
+// are Comm* (checked by magic).  Counts are in doubles.  Every rank issues the
+// same collectives in the same order.
+constexpr uint32_t kCommMagic = 0x4d46434du;  // "MFCM"
+struct Comm {
+  uint32_t magic = kCommMagic;
+  int rank = 0, size = 1;
+  virtual ~Comm() {}
+  virtual const char* kind() const = 0;
+  // in place: root's buf is the source, every other rank's buf receives it
+  virtual mf_status bcast(void* buf, size_t count, int root, cudaStream_t s) = 0;
+  // recv (root only) = sum over ranks of send; recv may equal send
+  virtual mf_status reduce(const double* send, double* recv, size_t count, int root,
+                           cudaStream_t s) = 0;
+  virtual mf_status allreduce(const double* send, double* recv, size_t count, cudaStream_t s) = 0;
+  // recv (recvcount) = sum over ranks of send[rank * recvcount ...]
+  virtual mf_status reduce_scatter(const double* send, double* recv, size_t recvcount,
+                                   cudaStream_t s) = 0;
+  // recv[k * sendcount ...] = send of rank k (send may be recv + rank * sendcount)
+  virtual mf_status allgather(const double* send, double* recv, size_t sendcount,
+                              cudaStream_t s) = 0;
+  virtual mf_status group_start() { return MF_OK; }
+  virtual mf_status group_end() { return MF_OK; }
+};
+Comm* comm_from(void* handle);  // nullptr if handle is not a Comm of this library
+
 // Largest flattened split factor P = p^levels the mix kernels are built for
 // (P^2 <= 81 blocks: p=9 one level, p=3 two levels, p=2 up to three levels).
 constexpr int kMaxBlocks = 81;
@@ -112,8 +142,15 @@ struct JitJob {
 int jit_build_all(const std::vector<JitJob>& jobs);
 void jit_free(MixTable& t);
 
+// kinds of K4/K6 launches counted per plan (mf_plan_kernels)
+enum MixKernelKind { MIXK_TABLE = 0, MIXK_FIXED = 1, MIXK_KRON = 2, MIXK_JIT = 3 };
+
 struct Plan {
   int device = 0;
+  // K4/K6 provenance: tables that asked for a generated kernel, kernels built,
+  // and launches per MixKernelKind since the plan was made
+  int jit_tables = 0, jit_built = 0;
+  mutable int64_t mix_launches[4] = {0, 0, 0, 0};
   int p = 1, R = 1, levels = 0;
   int64_t n = 0;
   // flattened triple: P = p^levels, RL = R^levels; U/V/W are P^2 x RL row-major
@@ -198,16 +235,21 @@ struct Plan {
   bool compute_pending = false;
   cudaStream_t cs1 = nullptr;
   int64_t async_calls = 0;
-  // NCCL
-  void* nccl_comm = nullptr;
+  // exchange (mf_options.comm): the communicator, MF_IN_ROOT
+  // replicas of A and B on ranks that receive them, and -- set by the
+  // host-buffer path for one call -- receive buffers used instead of them
+  Comm* comm = nullptr;
+  double *rA = nullptr, *rB = nullptr;
+  double *recvA = nullptr, *recvB = nullptr;
   cudaEvent_t done = nullptr;
   // level-by-level recursion (mf_options.level_by_level): the plan of each
   // leaf product (levels - 1 levels at n / p); this plan is then one level
   Plan* child = nullptr;
   // host-buffer pipeline (mf_dgemm_host): copy streams and per-slab events
   cudaStream_t h2d = nullptr, d2h = nullptr, mixs = nullptr, s2 = nullptr;
-  cudaStream_t comm = nullptr;   // region-overlapped NCCL reduces (comm_regions > 1)
-  std::vector<cudaEvent_t> comm_events;
+  cudaStream_t comm_s = nullptr;  // exchange stream: input broadcasts, region reduces
+  std::vector<cudaEvent_t> comm_events;  // region k computed (k < K), K4 done (K)
+  std::vector<cudaEvent_t> in_events;    // MF_IN_ROOT: A slab k landed, B slab k landed, all
   std::vector<cudaEvent_t> pipe_events;
   // phase profiling (mf_options.profile): 6 events per mf_dgemm call
   std::vector<std::vector<cudaEvent_t>> prof_events;

@@ -337,16 +337,19 @@ cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, in
   if (pl.fixed_id > 0 && own) {
     if (pl.shard_count > 1 && t.jit_fn) {  // a shard's own slots (see mf_plan)
       const cudaError_t j = jit_launch(t, X, ldx, out, pl.m, pl.m, 1.0, rows, 0, s);
-      if (j != cudaErrorNotSupported) return j;
+      if (j != cudaErrorNotSupported) return ++pl.mix_launches[MIXK_JIT], j;
     }
     const int side = &t == &pl.mixB ? 1 : 0;
     const ProdMask& mask = &t == &pl.mixA ? pl.mask_whole : (&t == &pl.mixA2 ? pl.mask_part : pl.mask_all);
-    if (pl.fixed_id >= 8) return launch_premix_kron(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
+    if (pl.fixed_id >= 8)
+      return ++pl.mix_launches[MIXK_KRON], launch_premix_kron(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
     if (fixed_vw4_ok(pl.m, X, ldx, out, pl.m))
-      return launch_premix_fixed(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
+      return ++pl.mix_launches[MIXK_FIXED],
+             launch_premix_fixed(pl.fixed_id, side, X, ldx, pl.m, out, s, rows, mask);
   }
   const cudaError_t j = jit_launch(t, X, ldx, out, pl.m, pl.m, 1.0, rows, 0, s);
-  if (j != cudaErrorNotSupported) return j;
+  if (j != cudaErrorNotSupported) return ++pl.mix_launches[MIXK_JIT], j;
+  ++pl.mix_launches[MIXK_TABLE];
   const int vw = pick_vw(pl.m, {{X, ldx}, {out, pl.m}});
   return mix_dispatch(vw, t, View{const_cast<double*>(X), ldx, pl.P}, View{out, pl.m, 0}, pl.m,
                       1.0, s, rows);
@@ -357,12 +360,15 @@ cudaError_t launch_postmix(const Plan& pl, const MixTable& t, double alpha, cons
   if (rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
   if (pl.fixed_id > 0 && !accumulate && (&t == &pl.mixC || &t == &pl.mixC2)) {
     const ProdMask& mask = &t == &pl.mixC ? pl.mask_whole : pl.mask_all;
-    if (pl.fixed_id >= 8) return launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
+    if (pl.fixed_id >= 8)
+      return ++pl.mix_launches[MIXK_KRON], launch_postmix_kron(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
     if (fixed_vw4_ok(pl.m, Pw, pl.m, C, ldc))
-      return launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
+      return ++pl.mix_launches[MIXK_FIXED],
+             launch_postmix_fixed(pl.fixed_id, Pw, pl.m, alpha, C, ldc, s, rows, mask);
   }
   const cudaError_t j = jit_launch(t, Pw, pl.m, C, ldc, pl.m, alpha, rows, accumulate ? 1 : 0, s);
-  if (j != cudaErrorNotSupported) return j;
+  if (j != cudaErrorNotSupported) return ++pl.mix_launches[MIXK_JIT], j;
+  ++pl.mix_launches[MIXK_TABLE];
   const int vw = pick_vw(pl.m, {{Pw, pl.m}, {C, ldc}});
   return mix_dispatch(vw, t, View{const_cast<double*>(Pw), pl.m, 0}, View{C, ldc, pl.P},
                       pl.m, alpha, s, rows, accumulate ? 1 : 0);

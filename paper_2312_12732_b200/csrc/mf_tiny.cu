@@ -203,7 +203,7 @@ size_t tiny_smem(const Plan& pl);
 
 bool tiny_eligible(const Plan& pl) {
   return pl.levels > 0 && pl.n <= 64 && pl.RL <= 64 && !pl.child && pl.batches.empty() &&
-         !pl.fuse && pl.shard_count == 1 && !pl.nccl_comm && pl.leaf == MF_LEAF_DMMA &&
+         !pl.fuse && pl.shard_count == 1 && !pl.comm && pl.leaf == MF_LEAF_DMMA &&
          pl.d_tinyU != nullptr && tiny_smem(pl) <= 200 * 1024;
 }
 

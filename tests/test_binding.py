@@ -281,3 +281,28 @@ def test_brent_check_rejects_coefficients_beyond_exact_range():
         M[M == 0] = 2.0 ** -30
     st, msg = _plan_status(2, 7, U, V, W, 1, 64, host_only=1)
     assert st == mf.MF_ERR_UNSUPPORTED and "exact Brent" in msg
+
+
+def test_loop_comm_handles_and_plan_validation():
+    """mf_loop_comm_create hands out one handle per in-process rank; a plan
+    with a communicator must shard as rank r of N (host-side checks only)."""
+    comms = mf.loop_comm_create(4)
+    try:
+        assert [mf.comm_info(c) for c in comms] == [
+            {"rank": r, "nranks": 4, "kind": "loopback"} for r in range(4)]
+        t = triples.STRASSEN_WINOGRAD
+        p = mf.Plan(t, 2, 512, host_only=True, comm=comms[2], shard_rank=2, shard_count=4)
+        assert (p.products()["shard"] == 2).sum() == 12
+        p.close()
+        st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 512, comm=comms[2].value, shard_rank=1,
+                               shard_count=4, host_only=1)
+        assert st == mf.MF_ERR_INVALID_ARG and "communicator" in msg
+        bogus = (ctypes.c_uint32 * 16)()
+        st, msg = _plan_status(2, 7, t.U, t.V, t.W, 1, 64, comm=ctypes.addressof(bogus), host_only=1)
+        assert st == mf.MF_ERR_INVALID_ARG and "mf_loop_comm_create" in msg
+        with pytest.raises(mf.MfError):
+            mf.loop_comm_create(17)
+    finally:
+        for c in comms:
+            mf.comm_destroy(c)
+    mf.comm_destroy(None)

@@ -332,6 +332,45 @@ def test_premix_postmix_compose_to_fmm():
         assert (T[q] == sum(t.U[k, q] * blocks[k] for k in range(4))).all()
 
 
+@pytest.mark.parametrize("name", ["strassen-winograd", "laderman"])
+@pytest.mark.parametrize("alpha", [3.0, -0.7, 0.1, -1.0, 0.0])
+def test_postmix_alpha_applied_once_after_the_sum(name, alpha):
+    """or_postmix's alpha branch (C = alpha*A*B; reading R8:
+    alpha once, after the W-sum).  Pins: (1) integer-valued P: equals alpha
+    times the block sums C_i = sum_q W[i][q] P_q done in exact int64
+    arithmetic; (2) random P: equals alpha * postmix(alpha=1) bitwise, while
+    applying alpha to every term (a plausible mistake) rounds differently --
+    the test shows it can tell the two apart; (3) alpha = 0 gives zeros."""
+    t = oracle.catalog(name)
+    p, R = t.p, t.R
+    m = 12
+    n = p * m
+    rng = np.random.Generator(np.random.PCG64(77))
+    Pi = rng.integers(-1000, 1001, size=(R, m, m)).astype(np.float64)
+    C = oracle.postmix(Pi, t, n, alpha)
+    Wi = t.W.astype(np.int64)
+    for i in range(p * p):
+        blk = C[(i // p) * m:(i // p + 1) * m, (i % p) * m:(i % p + 1) * m]
+        exact = sum(Wi[i, q] * Pi[q].astype(np.int64) for q in range(R))
+        assert (blk == alpha * exact.astype(np.float64)).all()
+    Pr = rng.uniform(-1, 1, size=(R, m, m))
+    C1 = oracle.postmix(Pr, t, n, 1.0)
+    Ca = oracle.postmix(Pr, t, n, alpha)
+    assert (Ca == alpha * C1).all()
+    if alpha in (0.1, -0.7):
+        per_term = np.zeros((n, n))
+        for i in range(p * p):
+            acc = None
+            for q in range(R):
+                if t.W[i, q] != 0:
+                    term = alpha * (t.W[i, q] * Pr[q])
+                    acc = term if acc is None else acc + term
+            per_term[(i // p) * m:(i // p + 1) * m, (i % p) * m:(i % p + 1) * m] = acc
+        assert (per_term != Ca).any()
+    if alpha == 0.0:
+        assert (Ca == 0).all()
+
+
 # ---------------------------------------------------------------- large-n helpers (O7)
 
 def test_freivalds_detects_planted_error():

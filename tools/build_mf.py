@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmf.so")
 
-SOURCES = ["mf_api.cpp", "mf_jit.cpp", "mf_mix.cu", "mf_fixed.cu", "mf_kron.cu", "mf_leaf.cu", "mf_tiny.cu"]
+SOURCES = ["mf_api.cpp", "mf_comm.cu", "mf_jit.cpp", "mf_mix.cu", "mf_fixed.cu", "mf_kron.cu", "mf_leaf.cu", "mf_tiny.cu"]
 HEADERS = ["mf_internal.h", "mf_tables.h", os.path.join("..", "..", "include", "mf.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
