@@ -630,13 +630,24 @@ def main():
         Cr = torch.matmul(Av, Bv)
         den = n * float(Av.abs().max()) * float(Bv.abs().max())
         out["variants"] = []
+        # the unfused SW^2 result on these inputs (flat K6; no split-K tail, which
+        # sums its pieces' k ranges separately): the ordered fold equals it bitwise
+        Cu = torch.empty((n, n), dtype=torch.float64, device=dev)
+        os.environ["MF_LEAF_SPLIT"] = "1"
+        plan.dgemm(Av, Bv, Cu)
+        torch.cuda.synchronize()
+        del os.environ["MF_LEAF_SPLIT"]
+        ordered = ("post-additions folded into the leaf epilogue in ascending q (ordered fold: "
+                   "bitwise the unfused result; no P workspace)")
         for label, levels, kw in (
                 (f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)", 3, {}),
+                (f"n={n} fp64, 3-level strassen-winograd, {ordered}", 3, {"fuse_postadd": 1}),
                 (f"n={n} fp64, 4-level strassen-winograd (one level by level, each of its 7 "
                  "products a flattened <8,8,8;343> child: 2401 leaves)", 4,
                  {"level_by_level": True, "recurse_levels": 1}),
-                (f"n={n} fp64, 2-level strassen-winograd, post-additions fused into the leaf "
-                 "epilogue (bulk f64 reductions into C, no P workspace)", 2, {"fuse_postadd": True}),
+                (f"n={n} fp64, 2-level strassen-winograd, {ordered}", 2, {"fuse_postadd": 1}),
+                (f"n={n} fp64, 2-level strassen-winograd, post-additions fused by bulk f64 "
+                 "reductions into C (order not fixed; no P workspace)", 2, {"fuse_postadd": 2}),
                 (f"n={n} fp64, 2-level strassen-winograd with cuBLAS-batched leaves (ablation: "
                  "same K4/K6, cublasDgemmBatched leaf)", 2, {"leaf": "cublas"})):
             if n % (2 ** levels):
@@ -654,12 +665,14 @@ def main():
                 vms = v0.elapsed_time(v1) / a.steps
                 ws = pv.info()["workspace_bytes"]
             errv = float((Cv - Cr).abs().max()) / den
-            out["variants"].append({
-                "workload": label, "value": 2.0 * n ** 3 / (vms * 1e-3) / 1e12, "unit": UNIT,
-                "ms_per_step": vms, "max_scaled_error": errv, "error_bound": 1e-13 * levels,
-                "workspace_gb": ws / 1e9,
-                "speedup_vs_cublas": (out.get("classical", {}).get("cublas_ms", 0) / vms) or None})
-        del Av, Bv, Cv, Cr
+            row = {"workload": label, "value": 2.0 * n ** 3 / (vms * 1e-3) / 1e12, "unit": UNIT,
+                   "ms_per_step": vms, "max_scaled_error_vs_cublas": errv,
+                   "error_bound": ceiling(levels), "workspace_gb": ws / 1e9,
+                   "speedup_vs_cublas": (out.get("classical", {}).get("cublas_ms", 0) / vms) or None}
+            if kw.get("fuse_postadd") == 1 and levels == 2:
+                row["bitwise_equal_unfused"] = bool(torch.equal(Cv, Cu))
+            out["variants"].append(row)
+        del Av, Bv, Cv, Cr, Cu
 
     if rank == 0 and world == 1 and not a.no_cpu:
         out["cpu_baseline"] = cpu_baseline(a)

@@ -103,20 +103,31 @@ typedef struct {
                            that fit (the paper's OOM at n=24012,
                            P:L489-492): per batch K4 on its slots, K5, K6 adding
                            into C.  Unsharded flattened plans only              */
-  int32_t fuse_postadd;   /* 1: fold the post-additions into the leaf epilogue
-                           (SURVEY §8a a4 / north_star (3): "optionally folded
-                           into the leaf GEMM epilogue so each product is
-                           accumulated straight into its C blocks").  C is
-                           zeroed, then every leaf tile adds alpha*W'[i][q]*P_q
-                           into each C block i it feeds with bulk f64 reductions
-                           (cp.reduce.async.bulk .add.f64).  No P workspace
-                           (saves R^L (n/p^L)^2 doubles); summation order across
-                           products is not fixed, so results are not bitwise
-                           reproducible (exact on integer-valued data within
-                           2^53).  Needs levels >= 1, flattened (not
-                           level_by_level) and no batching, else
-                           MF_ERR_UNSUPPORTED.  Odd ldc or C not 16-byte aligned
-                           run the simple leaf with f64 atomics instead       */
+  int32_t fuse_postadd;   /* fold the post-additions into the leaf epilogue (SURVEY
+                           §8a a4 / north_star (3): "optionally folded into the
+                           leaf GEMM epilogue so each product is accumulated
+                           straight into its C blocks"; no P workspace: saves
+                           R^L (n/p^L)^2 doubles).  Needs levels >= 1,
+                           flattened (not level_by_level), no batching, not
+                           the cuBLAS leaf, else MF_ERR_UNSUPPORTED.
+                           1 = ordered fold (SURVEY §8f NEXT-1 "deterministic
+                           product-serial ordering"): the leaf tiles at one
+                           position run in ascending q (a per-tile flag, tiles
+                           scheduled in ticket order); each stores
+                           W'[i][q]*P_q into C block i if q is the block's
+                           first product, else adds it to C_i, and applies
+                           alpha at the block's last product -- K6's
+                           per-element order, so C is bitwise the unfused
+                           result.  Unsharded plans only (MF_ERR_UNSUPPORTED
+                           otherwise).
+                           2 = bulk reductions: C is zeroed, then every leaf
+                           tile adds alpha*W'[i][q]*P_q into its C blocks with
+                           cp.reduce.async.bulk .add.f64; summation order
+                           across products not fixed (not bitwise
+                           reproducible; exact on integer data within 2^53).
+                           Odd ldc or C not 16-byte aligned run the simple
+                           leaf (f64 atomics for 2, one launch per product in
+                           order for 1)                                      */
   int32_t graph;          /* 1: mf_dgemm replays a CUDA graph of its launches.  The
                            first call with a given (A, lda, B, ldb, C, ldc,
                            alpha) runs eagerly; the second captures the step

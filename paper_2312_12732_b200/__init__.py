@@ -143,7 +143,7 @@ class Plan:
                  comm=None, nccl_comm=None, input_mode: int = IN_REPLICATED,
                  output_mode: int = OUT_ROOT,
                  profile: bool = False, host_only: bool = False, level_by_level: bool = False,
-                 max_workspace: int = 0, fuse_postadd: bool = False, recurse_levels: int = 0,
+                 max_workspace: int = 0, fuse_postadd: int = 0, recurse_levels: int = 0,
                  graph: bool = False, comm_regions: int = 0):
         self.triple, self.levels, self.n = triple, int(levels), int(n)
         opt = mf_options()
@@ -158,7 +158,7 @@ class Plan:
         opt.host_only = int(bool(host_only))
         opt.level_by_level = int(bool(level_by_level))
         opt.max_workspace = int(max_workspace)
-        opt.fuse_postadd = int(bool(fuse_postadd))
+        opt.fuse_postadd = int(fuse_postadd)  # True / 1: ordered fold; 2: bulk reductions
         opt.recurse_levels = int(recurse_levels)
         opt.graph = int(bool(graph))
         opt.comm_regions = int(comm_regions)

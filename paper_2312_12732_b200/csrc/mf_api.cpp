@@ -305,7 +305,7 @@ void free_plan(Plan* pl) {
                   (void*)pl->mixC2.d_table, (void*)pl->hA, (void*)pl->hB,
                   (void*)pl->d_post_off, (void*)pl->d_post, (void*)pl->d_ptrs, (void*)pl->Cfull,
                   (void*)pl->split_ws, (void*)pl->split_cnt, (void*)pl->d_tinyU, (void*)pl->d_tinyV,
-                  (void*)pl->rA, (void*)pl->rB,
+                  (void*)pl->rA, (void*)pl->rB, (void*)pl->fuse_sync,
                   (void*)pl->d_tinyW, (void*)pl->hA2, (void*)pl->hB2,
                   (void*)pl->hC2,
                   (void*)pl->hC})
@@ -435,7 +435,11 @@ mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B
   a.n_jobs = batch ? batch->n_jobs : (part ? pl.n_jobs_part : pl.n_jobs);
   if (batch) { a.n_slots_a = batch->n_a; a.n_slots_b = batch->n_b; }
   a.rows = rows;
-  if (pl.fuse && !batch && pl.levels > 0) { a.post_off = pl.d_post_off; a.post = pl.d_post; }
+  if (pl.fuse && !batch && pl.levels > 0) {
+    a.post_off = pl.d_post_off;
+    a.post = pl.d_post;
+    if (pl.fuse_ordered) { a.fuse_sync = pl.fuse_sync; a.fuse_sync_len = pl.fuse_sync_len; }
+  }
   if (pl.leaf == MF_LEAF_DMMA) {
     // split-K tail workspace: grown to what this launch's tiling needs
     const LeafTiles cfg = leaf_tiles(a);
@@ -513,6 +517,11 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     return fail(MF_ERR_UNSUPPORTED, "fuse_postadd needs levels >= 1");
   if (o.fuse_postadd && o.level_by_level && levels >= 2)
     return fail(MF_ERR_UNSUPPORTED, "fuse_postadd with level_by_level is not supported");
+  if (o.fuse_postadd < 0 || o.fuse_postadd > 2)
+    return fail(MF_ERR_INVALID_ARG, "fuse_postadd must be 0, 1 (ordered) or 2 (bulk reductions)");
+  if (o.fuse_postadd == 1 && o.shard_count > 1)
+    return fail(MF_ERR_UNSUPPORTED,
+                "fuse_postadd = 1 (ordered fold) needs an unsharded plan; sharded plans take 2");
   const int shard_count = o.shard_count > 1 ? o.shard_count : 1;
   if (o.shard_rank < 0 || o.shard_rank >= shard_count)
     return fail(MF_ERR_INVALID_ARG, "shard_rank %d outside [0, %d)", o.shard_rank, shard_count);
@@ -586,6 +595,7 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   pl->p = p; pl->R = R; pl->levels = levels; pl->n = n;
   pl->P = (int)P; pl->RL = RL; pl->m = n / P;
   pl->opt = o; pl->leaf = o.leaf; pl->fuse = o.fuse_postadd != 0;
+  pl->fuse_ordered = o.fuse_postadd == 1;
   pl->shard_rank = o.shard_rank; pl->shard_count = shard_count;
   pl->comm = comm_from(o.comm);
 
@@ -859,18 +869,49 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     std::vector<PostTerm> terms;
     std::vector<char> mine(RL, 0);
     for (int32_t q : job_q) mine[q] = 1;
+    // ordered fold: the first and last product (ascending q) feeding each C block
+    std::vector<int64_t> q_first(NB, -1), q_last(NB, -1);
+    for (int64_t q = 0; q < RL; ++q)
+      if (mine[q])
+        for (int i = 0; i < NB; ++i)
+          if (pl->W[i * RL + q] != 0.0) {
+            if (q_first[i] < 0) q_first[i] = q;
+            q_last[i] = q;
+          }
+    for (int i = 0; i < NB && pl->fuse_ordered; ++i)
+      if (q_first[i] < 0) {  // (a valid triple feeds every C block)
+        free_plan(pl.get());
+        return fail(MF_ERR_BAD_TRIPLE, "C block %d has no product (ordered fold)", i);
+      }
+    std::vector<int32_t> n_seen(NB, 0);
     for (int64_t q = 0; q < RL; ++q) {
       off[q] = (int32_t)terms.size();
       if (!mine[q]) continue;
       const size_t first = terms.size();
       for (int i = 0; i < NB; ++i) {
         const double w = pl->W[i * RL + q] * pl->prods[q].sign;
-        if (w != 0.0) terms.push_back(PostTerm{(int32_t)(((i / pl->P) << 16) | (i % pl->P)), 0, w});
+        if (w == 0.0) continue;
+        const int32_t fl = (q == q_first[i] ? POST_FIRST : 0) | (q == q_last[i] ? POST_LAST : 0) |
+                           (n_seen[i]++ << 8);  // ordered fold: the product's rank in block i
+        terms.push_back(PostTerm{(int32_t)(((i / pl->P) << 16) | (i % pl->P)), fl, w});
       }
-      std::stable_sort(terms.begin() + first, terms.end(),
-                       [](const PostTerm& x, const PostTerm& y) { return x.coef < y.coef; });
+      // the bulk-reduction fold restages its tile once per coefficient value
+      if (!pl->fuse_ordered)
+        std::stable_sort(terms.begin() + first, terms.end(),
+                         [](const PostTerm& x, const PostTerm& y) { return x.coef < y.coef; });
     }
     off[RL] = (int32_t)terms.size();
+    if (pl->fuse_ordered) {
+      // per-tile-position flags of the widest tiling (64-wide tiles), then the
+      // ticket and done counters; zero between launches
+      const int64_t tiles = (int64_t)NB * ((pl->m + 127) / 128) * ((pl->m + 63) / 64);
+      pl->fuse_sync_len = tiles;
+      if (cudaMalloc(&pl->fuse_sync, sizeof(uint32_t) * (tiles + 2)) != cudaSuccess ||
+          cudaMemset(pl->fuse_sync, 0, sizeof(uint32_t) * (tiles + 2)) != cudaSuccess) {
+        free_plan(pl.get());
+        return fail(MF_ERR_OUT_OF_MEMORY, "ordered fold flags");
+      }
+    }
     if (cudaMalloc(&pl->d_post_off, sizeof(int32_t) * off.size()) != cudaSuccess ||
         (!terms.empty() && cudaMalloc(&pl->d_post, sizeof(PostTerm) * terms.size()) != cudaSuccess)) {
       free_plan(pl.get());
@@ -1190,10 +1231,12 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
       MF_CUDA(launch_postmix(*pl, b.mixC, alpha, pl->Pw, C, ldc, s, Rows(), bi > 0), "post-add (K6, batch)");
     }
   } else if (pl->fuse) {
-    // fused post-addition: C = 0, then K4(A), K4(B) and the leaf, whose epilogue
-    // adds alpha * W'[i][q] * P_q into each C block i (no K6, no P workspace)
-    // (profile: the memset is timed with pre-add A)
-    MF_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, n * 8, n, s), "zero C");
+    // fused post-addition: K4(A), K4(B) and the leaf, whose epilogue folds
+    // W'[i][q] * P_q into each C block i (no K6, no P workspace).  Ordered
+    // (fuse_postadd = 1): each tile position's products update C in ascending
+    // q -- store first, add, alpha last: bitwise K6.  Bulk reductions (2): C
+    // is zeroed first (profile: timed with pre-add A), order not fixed.
+    if (!pl->fuse_ordered) MF_CUDA(cudaMemset2DAsync(C, ldc * 8, 0, n * 8, n, s), "zero C");
     if ((st = premix_side(0)) != MF_OK) return st;
     mark(1);
     if ((st = premix_side(1)) != MF_OK) return st;

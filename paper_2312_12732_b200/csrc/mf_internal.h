@@ -76,10 +76,14 @@ struct LeafJob {
 // Fused post-addition (mf_options.fuse_postadd): product q's tiles are added
 // into C blocks post[post_off[q] .. post_off[q+1]) with coef*alpha; terms of one
 // product are sorted by coef so the epilogue restages its tile once per value.
+// Ordered fold (fuse_postadd = 1): flags mark the product that writes C block
+// i first (store, no load) and last (alpha applied) in ascending q; bits 8..
+// hold the product's rank among block i's products (the flag value it waits for).
+enum PostFlags : int32_t { POST_FIRST = 1, POST_LAST = 2 };
 struct PostTerm {
-  int32_t blk;   // (block_row << 16) | block_col of the C block
-  int32_t pad;
-  double coef;   // W'[i][q] with the alias sign folded in
+  int32_t blk;    // (block_row << 16) | block_col of the C block
+  int32_t flags;  // PostFlags (ordered fold only)
+  double coef;    // W'[i][q] with the alias sign folded in
 };
 
 // Coefficient table of one mix kernel launch: nout outputs, each a
@@ -188,7 +192,10 @@ struct Plan {
   double* T = nullptr;   // n_mat_a x m x m
   double* S = nullptr;   // n_mat_b x m x m
   double* Pw = nullptr;  // RL x m x m (leaf outputs; not allocated when fused)
-  bool fuse = false;     // mf_options.fuse_postadd
+  bool fuse = false;     // mf_options.fuse_postadd != 0
+  bool fuse_ordered = false;  // fuse_postadd == 1: deterministic ordered fold
+  uint32_t* fuse_sync = nullptr;  // ordered fold: per-tile flags, ticket, done counter
+  int64_t fuse_sync_len = 0;      // flags (tiles of the widest tiling)
   int32_t* d_post_off = nullptr;  // RL + 1
   PostTerm* d_post = nullptr;
   size_t ws_bytes = 0;
@@ -301,6 +308,11 @@ struct LeafArgs {
   // (ldc) per post[post_off[out_idx] ..) instead of stored to out
   const int32_t* post_off = nullptr;
   const PostTerm* post = nullptr;
+  // ordered fold (fuse_postadd = 1): products of one tile position update C
+  // in job (= ascending q) order; flags[tiles] + ticket + done counter,
+  // zero between launches (the kernel's last CTA resets them)
+  uint32_t* fuse_sync = nullptr;
+  int64_t fuse_sync_len = 0;
   // split-K tail workspace (plan-owned; sized from leaf_tiles): partial tiles
   // and per-tail-tile arrival counters (zero between launches)
   double* split_ws = nullptr;

@@ -103,8 +103,13 @@ struct LeafParams {
   int64_t ldo, out_stride;
   double alpha;
   const LeafJob* jobs;
-  const int32_t* post_off;  // fused post-addition (FUSE): out = C, ldo = ldc
+  const int32_t* post_off;  // fused post-addition (FUSE > 0): out = C, ldo = ldc
   const PostTerm* post;
+  // ordered fold (FUSE == 2): flags[P*P][tiles_m * tiles_n] (per C block and
+  // tile position: how many of the block's products have updated it), then
+  // the ticket and done counters
+  uint32_t* sync;
+  int nP;
   // split-K tail: blocks >= n_whole are pieces (tile n_whole + (b - n_whole) / split,
   // k-range (b - n_whole) % split); partials in part_ws, arrivals in part_cnt
   int n_whole, split;
@@ -168,10 +173,29 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// L2-coherent loads of C in the ordered fold (another SM wrote it since this
+// SM may last have cached it): ld.global.cg
+__device__ __forceinline__ void ldcg_v2(const double* p, double& x, double& y) {
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
+}
+
 // BNT = CTA tile width (128, or 64 to cut wave quantisation on small batches):
 // warps form a 2 x 4 grid of 64 x (BNT/4) warp tiles, NJ = BNT/64 16-column
-// groups per warp.
-template <int BNT, int KSUB, bool FUSE>
+// groups per warp.  FUSE: 0 = store P_q' (then K6), 1 = fused post-addition by
+// bulk f64 reductions into C (order not fixed), 2 = ordered fold: the products
+// of one tile position update C in job order (ascending q), store / add /
+// alpha-last exactly as K6, so C is bitwise the unfused result.
+template <int BNT, int KSUB, int FUSE>
 __global__ void __launch_bounds__(THREADS, 1)
 leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
@@ -189,10 +213,20 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const uint32_t empty0 = full0 + STAGES * 8;
 
   // ---- block -> tile (whole, or one k-range piece of a tail tile) ----
-  const bool piece = !FUSE && prm.split > 1 && (int)blockIdx.x >= prm.n_whole;
-  int tile = blockIdx.x, split_idx = 0, kb0 = 0, nk = prm.kblocks;
+  // ordered fold: tiles in ticket order, so the CTA a tile waits for (same
+  // position, previous product) has started -- forward progress by induction
+  int block = blockIdx.x;
+  if constexpr (FUSE == 2) {
+    __shared__ int s_ticket;
+    if (threadIdx.x == 0)
+      s_ticket = (int)atomicAdd(prm.sync + prm.nP * prm.nP * prm.tiles_m * prm.tiles_n, 1u);
+    __syncthreads();
+    block = s_ticket;
+  }
+  const bool piece = !FUSE && prm.split > 1 && block >= prm.n_whole;
+  int tile = block, split_idx = 0, kb0 = 0, nk = prm.kblocks;
   if (piece) {
-    const int pc = blockIdx.x - prm.n_whole;
+    const int pc = block - prm.n_whole;
     tile = prm.n_whole + pc / prm.split;
     split_idx = pc % prm.split;
     kb0 = split_idx * prm.kblocks / prm.split;
@@ -354,7 +388,102 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     }
   }
 
-  if constexpr (FUSE) {
+  if constexpr (FUSE == 2) {
+    // ---- ordered fold (north_star (3); SURVEY §8f NEXT-1 "deterministic
+    // product-serial ordering"): for every C block i this product feeds, wait
+    // until the block's previous products have updated this tile position,
+    // then C_i = W'[i][q] * P (first product of block i) or C_i + W'[i][q] * P,
+    // times alpha at the last product -- K6's per-element order exactly ----
+    const int tiles = prm.tiles_m * prm.tiles_n;
+    const int nflags = prm.nP * prm.nP * tiles;
+    const int q = job.out_idx;
+    const int t0 = prm.post_off[q], t1 = prm.post_off[q + 1];
+    const double alpha = prm.alpha;
+    // 256-bit stores need every C block's column offset (bc * m) 4-aligned too
+    const bool vec_ok = ((prm.ldo & 3) == 0) && ((prm.m & 3) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(prm.out) & 31) == 0);
+    for (int ti = t0; ti < t1; ++ti) {
+      const PostTerm pt = prm.post[ti];
+      const int br = pt.blk >> 16, bc = pt.blk & 0xffff;
+      const int seq = pt.flags >> 8;  // products of block i before this one
+      uint32_t* flag = prm.sync + (int64_t)(br * prm.nP + bc) * tiles + t;
+      if (threadIdx.x == 0 && seq > 0)
+        while (ld_acquire(flag) < (uint32_t)seq) __nanosleep(64);
+      __syncthreads();
+      const double w = pt.coef;
+      const bool first = pt.flags & POST_FIRST;
+      const bool scale = (pt.flags & POST_LAST) && alpha != 1.0;
+      double* cb = prm.out + (int64_t)br * prm.m * prm.ldo + (int64_t)bc * prm.m;
+      // the warp tile in HALVES row groups: each group's loads are all in
+      // flight before its first add (128-wide tiles: two groups of 4 x 16
+      // rows, 32 registers of C per thread -- a whole tile would spill)
+      constexpr int HALVES = NJ == 2 ? 2 : 1, MH = 8 / HALVES;
+#pragma unroll
+      for (int h = 0; h < HALVES; ++h) {
+        double old[MH][NJ][4];
+        if (!first) {
+#pragma unroll
+          for (int mh = 0; mh < MH; ++mh) {
+            const int mi = MH * h + mh;
+            const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
+#pragma unroll
+            for (int nj = 0; nj < NJ; ++nj) {
+              const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
+              const double* src = cb + row * prm.ldo + col;
+              if (row < prm.m && vec_ok && col + 3 < prm.m) {
+                ldcg_v2(src, old[mh][nj][0], old[mh][nj][1]);
+                ldcg_v2(src + 2, old[mh][nj][2], old[mh][nj][3]);
+              } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  old[mh][nj][u] = (row < prm.m && col + u < prm.m) ? __ldcg(src + u) : 0.0;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int mh = 0; mh < MH; ++mh) {
+          const int mi = MH * h + mh;
+          const int64_t row = (int64_t)tm * BM + wm * 64 + mi * 8 + lr;
+          if (row >= prm.m) continue;
+#pragma unroll
+          for (int nj = 0; nj < NJ; ++nj) {
+            const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
+            double v[4] = {__dmul_rn(w, acc[mi][nj][0][0]), __dmul_rn(w, acc[mi][nj][1][0]),
+                           __dmul_rn(w, acc[mi][nj][0][1]), __dmul_rn(w, acc[mi][nj][1][1])};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (!first) v[u] = __dadd_rn(old[mh][nj][u], v[u]);
+              if (scale) v[u] = __dmul_rn(alpha, v[u]);
+            }
+            double* dst = cb + row * prm.ldo + col;
+            if (vec_ok && col + 3 < prm.m) {
+              asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
+                           :: "l"(dst), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]) : "memory");
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (col + u < prm.m) dst[u] = v[u];
+            }
+          }
+        }
+      }
+      // publish: block i's tile is updated through this product
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(flag, (uint32_t)seq + 1);
+      }
+    }
+    __shared__ int s_last;
+    if (threadIdx.x == 0) s_last = atomicAdd(prm.sync + nflags + 1, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {  // every CTA is done: zero the flags and counters for the next launch
+      for (int i = threadIdx.x; i < nflags; i += THREADS) prm.sync[i] = 0;
+      if (threadIdx.x == 0) { prm.sync[nflags] = 0; prm.sync[nflags + 1] = 0; }
+    }
+    return;
+  } else if constexpr (FUSE == 1) {
     // ---- fused post-addition (north_star (3), "folded into the leaf GEMM
     // epilogue"): stage coef*alpha*acc in the drained ring, then threads
     // 0..127 each add one tile row into every C block product q feeds with a
@@ -490,6 +619,7 @@ struct SimpleParams {
   const LeafJob* jobs;
   const int32_t* post_off;  // fused post-addition: out = C, ldo = ldc
   const PostTerm* post;
+  int ordered;  // ordered fold: one launch per job, in job order (stream-ordered)
 };
 
 __global__ void leaf_simple_kernel(const SimpleParams prm) {
@@ -512,7 +642,15 @@ __global__ void leaf_simple_kernel(const SimpleParams prm) {
     for (int t = prm.post_off[job.out_idx]; t < prm.post_off[job.out_idx + 1]; ++t) {
       const PostTerm pt = prm.post[t];
       const int64_t br = pt.blk >> 16, bc = pt.blk & 0xffff;
-      atomicAdd(prm.out + (br * prm.m + r) * prm.ldo + bc * prm.m + c, pt.coef * prm.alpha * acc);
+      double* dst = prm.out + (br * prm.m + r) * prm.ldo + bc * prm.m + c;
+      if (prm.ordered) {  // K6's order: store first, add, alpha last
+        double v = __dmul_rn(pt.coef, acc);
+        if (!(pt.flags & POST_FIRST)) v = __dadd_rn(*dst, v);
+        if ((pt.flags & POST_LAST) && prm.alpha != 1.0) v = __dmul_rn(prm.alpha, v);
+        *dst = v;
+      } else {
+        atomicAdd(dst, pt.coef * prm.alpha * acc);
+      }
     }
     return;
   }
@@ -646,8 +784,10 @@ LeafTiles leaf_tiles(const LeafArgs& a) {
 cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
   const int64_t r0 = a.rows.r0, r1 = a.rows.end(a.m), c0 = a.rows.c0, c1 = a.rows.cend(a.m);
   if (a.n_jobs == 0 || a.m == 0 || r1 <= r0 || c1 <= c0) return cudaSuccess;
-  // fused post-addition: bulk reductions need 16-byte aligned C rows
-  const bool fuse_ok = !a.post || (!(a.ldo & 1) && al16(a.out));
+  // fused post-addition: bulk reductions need 16-byte aligned C rows (the
+  // ordered fold stores from registers: any 8-byte aligned C)
+  const bool ordered = a.post && a.fuse_sync;
+  const bool fuse_ok = !a.post || ordered || (!(a.ldo & 1) && al16(a.out));
   if (leaf_kind == MF_LEAF_DMMA && leaf_tma_supported(a) && fuse_ok && r0 % BM == 0 &&
       c0 % BN == 0 && (c1 == a.m || c1 % BN == 0)) {
     const int64_t tm_tiles = (r1 - r0 + BM - 1) / BM;
@@ -666,6 +806,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (ksub == 3 && bn != 128) ksub = 2;
     const bool fuse = a.post != nullptr;
     if (fuse) ksub = 2;  // the fused tile is staged in the KSUB=2 ring
+    if (ordered &&
+        (int64_t)a.P * a.P * ((r1 - r0 + BM - 1) / BM) * ((c1 - c0 + bn - 1) / bn) > a.fuse_sync_len)
+      return cudaErrorInvalidValue;
     CUtensorMap mA, mT, mB, mS;
     const bool ok =
         encode_block_view(&mA, a.A, a.lda, a.P, a.m, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) &&
@@ -687,6 +830,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.jobs = a.jobs;
     prm.post_off = a.post_off;
     prm.post = a.post;
+    prm.sync = a.fuse_sync;
+    // prefetch the C tiles ~8 stages (256 k) before the end of the k loop
+    prm.nP = a.P;
     prm.split = cfg.split;
     prm.n_whole = cfg.split > 1 ? (int)cfg.n_whole : 0;
     prm.part_ws = a.split_ws;
@@ -698,9 +844,10 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)
-    static std::atomic<uint64_t> attr_set[7];
-    const int inst = fuse ? (bn == 64 ? 5 : 4)
-                          : (ksub == 3 ? 6 : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0));
+    static std::atomic<uint64_t> attr_set[9];
+    const int inst = ordered ? (bn == 64 ? 8 : 7)
+                     : fuse  ? (bn == 64 ? 5 : 4)
+                             : (ksub == 3 ? 6 : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0));
     const uint64_t dev_bit = 1ull << (dev & 63);
     auto launch = [&](auto kern, int smem) -> cudaError_t {
       if (!(attr_set[inst].load() & dev_bit)) {
@@ -713,19 +860,29 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     };
     cudaError_t e;
     switch (inst) {
-      case 0: e = launch(leaf_dmma_kernel<128, 1, false>, smem_bytes<128, 1>()); break;
-      case 1: e = launch(leaf_dmma_kernel<128, 2, false>, smem_bytes<128, 2>()); break;
-      case 2: e = launch(leaf_dmma_kernel<64, 1, false>, smem_bytes<64, 1>()); break;
-      case 3: e = launch(leaf_dmma_kernel<64, 2, false>, smem_bytes<64, 2>()); break;
-      case 4: e = launch(leaf_dmma_kernel<128, 2, true>, smem_bytes<128, 2>()); break;
-      case 6: e = launch(leaf_dmma_kernel<128, 3, false>, smem_bytes<128, 3>()); break;
-      default: e = launch(leaf_dmma_kernel<64, 2, true>, smem_bytes<64, 2>()); break;
+      case 0: e = launch(leaf_dmma_kernel<128, 1, 0>, smem_bytes<128, 1>()); break;
+      case 1: e = launch(leaf_dmma_kernel<128, 2, 0>, smem_bytes<128, 2>()); break;
+      case 2: e = launch(leaf_dmma_kernel<64, 1, 0>, smem_bytes<64, 1>()); break;
+      case 3: e = launch(leaf_dmma_kernel<64, 2, 0>, smem_bytes<64, 2>()); break;
+      case 4: e = launch(leaf_dmma_kernel<128, 2, 1>, smem_bytes<128, 2>()); break;
+      case 6: e = launch(leaf_dmma_kernel<128, 3, 0>, smem_bytes<128, 3>()); break;
+      case 7: e = launch(leaf_dmma_kernel<128, 2, 2>, smem_bytes<128, 2>()); break;
+      case 8: e = launch(leaf_dmma_kernel<64, 2, 2>, smem_bytes<64, 2>()); break;
+      default: e = launch(leaf_dmma_kernel<64, 2, 1>, smem_bytes<64, 2>()); break;
     }
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
   SimpleParams prm{a.A, a.B, a.T, a.S, a.lda, a.ldb, a.m, r0, r1, c0, c1, a.out, a.ldo,
-                   a.out_block_stride, a.alpha, a.jobs, a.post_off, a.post};
+                   a.out_block_stride, a.alpha, a.jobs, a.post_off, a.post, ordered ? 1 : 0};
+  if (ordered) {  // one launch per product, in order (the stream serialises them)
+    dim3 grid((unsigned)((c1 - c0 + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), 1);
+    for (int j = 0; j < a.n_jobs; ++j) {
+      prm.jobs = a.jobs + j;
+      leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
+    }
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((c1 - c0 + 15) / 16), (unsigned)((r1 - r0 + 15) / 16), (unsigned)a.n_jobs);
   leaf_simple_kernel<<<grid, dim3(16, 16), 0, s>>>(prm);
   return cudaGetLastError();

@@ -182,6 +182,14 @@ def test_fused_postadd_option_validation():
     p = mf.Plan(t, 2, 64, fuse_postadd=True, host_only=True)
     assert p.info()["n_products"] == 49
     p.close()
+    # the ordered fold (1) is for unsharded plans; sharded plans take the
+    # bulk-reduction fold (2); other values are refused
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, fuse_postadd=1, shard_count=2, host_only=1)
+    assert st == mf.MF_ERR_UNSUPPORTED and "ordered" in msg
+    p = mf.Plan(t, 2, 64, fuse_postadd=2, shard_count=2, shard_rank=1, host_only=True)
+    p.close()
+    st, msg = _plan_status(2, 7, t.U, t.V, t.W, 2, 64, fuse_postadd=3, host_only=1)
+    assert st == mf.MF_ERR_INVALID_ARG and "fuse_postadd" in msg
 
 
 def test_output_mode_and_leaf_validation():

@@ -674,30 +674,68 @@ FUSED_CASES = [(SW, 1, 256), (SW, 1, 400), (SW, 2, 512), (SW, 2, 800), (SW, 3, 1
                ("laderman", 2, 288), ("classical-p2", 1, 128)]
 
 
+def _ordered_and_flat(monkeypatch, t, levels, n, A, B, alpha, **kw):
+    """(ordered fold, unfused) results with the same flat-order kernels: both
+    plans use the flat ascending-index K4 (generated / table kernels; the
+    Kronecker-factored K4/K6 of deep catalog powers sum in the recursion's
+    order instead), and the unfused leaf has no split-K tail (a split tile sums
+    its k range in pieces).  The ordered fold must then equal K5 + K6 bitwise."""
+    with monkeypatch.context() as mp:
+        mp.setenv("MF_MIX_GENERIC", "1")
+        mp.setenv("MF_LEAF_SPLIT", "1")
+        with mf.Plan(t, levels, n, fuse_postadd=1, **kw) as p:
+            Cf = host(p.dgemm(dev(A), dev(B), alpha=alpha))
+        with mf.Plan(t, levels, n, **kw) as p:
+            Cu = host(p.dgemm(dev(A), dev(B), alpha=alpha))
+    return Cf, Cu
+
+
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("name,levels,n", FUSED_CASES)
-def test_fused_postadd_integer_exact_and_random(name, levels, n):
+def test_fused_postadd_integer_exact_and_random(name, levels, n, mode, monkeypatch):
     """North_star (3) / SURVEY §8a a4 "optionally folded into the leaf GEMM
-    epilogue": every product tile is added (bulk f64 reductions) into the C
-    blocks it feeds.  Integers: bit-exact (all partial sums exact, so order is
-    irrelevant); random: within the bound and close to the unfused path.
-    Covers -1 coefficients (restaged tile), ragged tails (n=400: m=200, n=800:
-    m=200, n=390: m=130), alpha != 1, and no P workspace."""
+    epilogue": every product tile goes straight into the C blocks it feeds.
+    Mode 1, the ordered fold (SURVEY §8f NEXT-1 "deterministic product-serial
+    ordering"): tiles of one position update C in ascending q, store / add /
+    alpha last like K6 -- bitwise the unfused path on random inputs, and
+    bitwise from run to run.  Mode 2 (bulk f64 reductions, order not fixed):
+    integers bit-exact (all partial sums exact); random within the bound.
+    Covers -1 coefficients, ragged tails (n=400: m=200, n=800: m=200, n=390:
+    m=130), alpha != 1, NaN-filled C (write-only), no P workspace."""
     t = triples.get(name)
     A, B = mf_inputs.pair("int1024", n, 40)
-    with mf.Plan(t, levels, n, fuse_postadd=True) as p:
+    with mf.Plan(t, levels, n, fuse_postadd=mode) as p:
         C = torch.full((n, n), float("nan"), dtype=torch.float64, device="cuda")
         assert (host(p.dgemm(dev(A), dev(B), C=C)) == exact(A, B)).all()
         assert (host(p.dgemm(dev(A), dev(B), alpha=-2.0)) == -2.0 * exact(A, B)).all()
         A, B = mf_inputs.pair("uniform", n, 41)
         Cf = host(p.dgemm(dev(A), dev(B), alpha=0.5))
-    with mf.Plan(t, levels, n) as p:
-        Cu = host(p.dgemm(dev(A), dev(B), alpha=0.5))
+        Cf2 = host(p.dgemm(dev(A), dev(B), alpha=0.5))
     Cref = 0.5 * oracle.classical(A, B)
     assert_error(scaled(Cf, Cref, A, B), levels)
-    assert_error(scaled(Cf, Cu, A, B), levels)
+    if mode == 1:
+        assert (Cf2 == Cf).all()  # deterministic
+        Co, Cu = _ordered_and_flat(monkeypatch, t, levels, n, A, B, 0.5)
+        assert (Co == Cu).all()
+    else:
+        with mf.Plan(t, levels, n) as p:
+            assert_error(scaled(Cf, host(p.dgemm(dev(A), dev(B), alpha=0.5)), A, B), levels)
 
 
-def test_fused_postadd_workspace_views_and_fallbacks():
+@pytest.mark.parametrize("name,levels,n", [(SW, 3, 1024), ("laderman", 1, 768), (SW, 1, 4096),
+                                           ("paper-strassen", 2, 1000)])
+def test_fused_ordered_bitwise_unfused(name, levels, n, monkeypatch):
+    """The ordered fold at more shapes: SW^3 (343 products, ~5 C blocks per
+    product), Laderman (p = 3), one level at a bench size (7 products of
+    2048^2), a ragged leaf (m = 250): C bitwise the unfused K5 + flat K6 result
+    (itself bitwise or_postmix, test_postmix_bit_exact)."""
+    t = triples.get(name)
+    A, B = mf_inputs.pair("uniform", n, 46)
+    Cf, Cu = _ordered_and_flat(monkeypatch, t, levels, n, A, B, -1.25)
+    assert (Cf == Cu).all()
+
+
+def test_fused_postadd_workspace_views_and_fallbacks(monkeypatch):
     """Fused plans allocate no P workspace; strided C (ldc > n, even) keeps the
     TMA/bulk path, odd ldc falls back to the simple leaf with f64 atomics; the
     simple leaf kind and the host-buffer entry point work fused too."""
@@ -707,16 +745,27 @@ def test_fused_postadd_workspace_views_and_fallbacks():
         ws_unfused = p.info()["workspace_bytes"]
     A, B = mf_inputs.pair("int1024", n, 42)
     ref = exact(A, B)
-    with mf.Plan(t, 2, n, fuse_postadd=True) as p:
-        assert ws_unfused - p.info()["workspace_bytes"] == 49 * m * m * 8
-        for ldc in (n + 2, n + 1):
-            Cbig = torch.full((n, ldc), 7.0, dtype=torch.float64, device="cuda")
-            p.dgemm(dev(A), dev(B), C=Cbig[:, :n])
-            out = host(Cbig)
-            assert (out[:, :n] == ref).all() and (out[:, n:] == 7.0).all()
-        assert (p.dgemm_host(A, B) == ref).all()
-    with mf.Plan(t, 2, n, fuse_postadd=True, leaf="simple") as p:
-        assert (host(p.dgemm(dev(A), dev(B))) == ref).all()
+    for mode in (1, 2):
+        with mf.Plan(t, 2, n, fuse_postadd=mode) as p:
+            assert ws_unfused - p.info()["workspace_bytes"] == 49 * m * m * 8
+            for ldc in (n + 2, n + 1):
+                Cbig = torch.full((n, ldc), 7.0, dtype=torch.float64, device="cuda")
+                p.dgemm(dev(A), dev(B), C=Cbig[:, :n])
+                out = host(Cbig)
+                assert (out[:, :n] == ref).all() and (out[:, n:] == 7.0).all()
+            assert (p.dgemm_host(A, B) == ref).all()
+        with mf.Plan(t, 2, n, fuse_postadd=mode, leaf="simple") as p:
+            assert (host(p.dgemm(dev(A), dev(B))) == ref).all()
+    # the ordered fold on the simple leaf (one launch per product, in order) and
+    # on odd ldc (scalar stores) is bitwise the unfused result on random inputs
+    A, B = mf_inputs.pair("uniform", n, 47)
+    Cs, Cu = _ordered_and_flat(monkeypatch, t, 2, n, A, B, 3.0, leaf="simple")
+    assert (Cs == Cu).all()
+    _, Cu = _ordered_and_flat(monkeypatch, t, 2, n, A, B, 3.0)
+    with mf.Plan(t, 2, n, fuse_postadd=1) as p:
+        Cbig = torch.full((n, n + 1), 7.0, dtype=torch.float64, device="cuda")
+        p.dgemm(dev(A), dev(B), C=Cbig[:, :n], alpha=3.0)
+        assert (host(Cbig)[:, :n] == Cu).all()
 
 
 @pytest.mark.parametrize("N", [1, 3])
@@ -728,16 +777,17 @@ def test_fused_postadd_sharded_partials(N):
     Ad, Bd = dev(A), dev(B)
     total = torch.zeros((n, n), dtype=torch.float64, device="cuda")
     for r in range(N):
-        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N, fuse_postadd=True) as p:
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N, fuse_postadd=2) as p:
             total += p.dgemm(Ad, Bd)
     assert (host(total) == exact(A, B)).all()
 
 
 def test_fused_postadd_bench_size_sampled():
-    """n = 16384, SW^2 fused (the bench's --fuse variant): Freivalds on integers
-    is exact; random inputs checked on sampled oracle entries."""
+    """n = 16384, SW^2 fused (the bench's --fuse variant, ordered fold):
+    Freivalds on integers is exact; random inputs checked on sampled oracle
+    entries."""
     n = 16384
-    with mf.Plan(triples.get(SW), 2, n, fuse_postadd=True) as p:
+    with mf.Plan(triples.get(SW), 2, n, fuse_postadd=1) as p:
         Ad, Bd = mf_inputs.device_pair("int1024", n, 44)
         C = host(p.dgemm(Ad, Bd))
         A, B = host(Ad), host(Bd)
@@ -936,7 +986,8 @@ def test_three_level_sharding_n8(regions):
 @pytest.mark.parametrize("name,levels,n,kw", [(SW, 2, 2048, {}), (SW, 1, 1000, {}), (None, 0, 1024, {}),
                                               (SW, 2, 1024, {"level_by_level": True}),
                                               (SW, 3, 1024, {"level_by_level": True, "recurse_levels": 1}),
-                                              (SW, 2, 1024, {"fuse_postadd": True}),
+                                              (SW, 2, 1024, {"fuse_postadd": 1}),
+                                              (SW, 2, 1024, {"fuse_postadd": 2}),
                                               (SW, 2, 512, {"max_workspace": 3 * 5 * 128 * 128 * 8}),
                                               (SW, 2, 512, {"leaf": "cublas"})])
 def test_host_async_stream_matches_sync(name, levels, n, kw):
@@ -960,14 +1011,14 @@ def test_host_async_stream_matches_sync(name, levels, n, kw):
             p.dgemm_host_async_ptr(Ah.data_ptr(), n, Bh.data_ptr(), n, Ch.data_ptr(), n, alpha=0.5)
         p.host_sync()
         for (Ah, Bh), Ch, ref in zip(ins, outs, refs):
-            if kw.get("fuse_postadd"):  # bulk-reduction order varies run to run: the bound
+            if kw.get("fuse_postadd") == 2:  # bulk-reduction order varies run to run: the bound
                 assert scaled(Ch.numpy(), ref, Ah.numpy(), Bh.numpy()) <= 1e-15
             else:
                 assert (Ch.numpy() == ref).all()
         Ai, Bi = mf_inputs.pair("int1024", n, 80)
         p.dgemm_host_async_ptr(ins[0][0].data_ptr(), n, ins[0][1].data_ptr(), n, outs[0].data_ptr(), n)
         assert (p.dgemm_host(Ai, Bi) == exact(Ai, Bi)).all()  # drains the async call first
-        if kw.get("fuse_postadd"):
+        if kw.get("fuse_postadd") == 2:
             assert scaled(outs[0].numpy(), 2.0 * refs[0], ins[0][0].numpy(), ins[0][1].numpy()) <= 1e-15
         else:
             assert (outs[0].numpy() == 2.0 * refs[0]).all()

@@ -195,7 +195,7 @@ def test_loopback_level_by_level_and_fused():
     fused post-addition, exchanged across 3 loopback ranks."""
     n = 1024
     A, B, ref = inputs("int1024", n, 9)
-    for kw in ({"level_by_level": True}, {"fuse_postadd": True}):
+    for kw in ({"level_by_level": True}, {"fuse_postadd": 2}):
         comms = mf.loop_comm_create(3)
         res, errs = [None] * 3, []
 
