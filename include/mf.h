@@ -177,7 +177,10 @@ typedef struct {
 mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const double* V,
                   const double* W, int32_t levels, int64_t n, const mf_options* opt);
 
-/* mf_dgemm -- C <- alpha * A * B through the planned algorithm.
+/* mf_dgemm -- C <- alpha * A * B through the planned algorithm: the problem
+ * statement C = alpha A B (§3) computed as Eq. "strassen"
+ * (L196-203): T_q, S_q pre-additions, the R^L products P_q, the
+ * post-additions C_i (order of terms: DESIGN.md R7/R8).
  * A (n x n, lda), B (n x n, ldb): device, read-only.  C (n x n, ldc): device,
  * write-only (BLAS beta = 0: prior contents, even NaN, are ignored); C must
  * not overlap A or B (MF_ERR_INVALID_ARG).  Launches, in stream order:
@@ -190,7 +193,8 @@ mf_status mf_plan(mf_plan_t* out, int32_t p, int32_t R, const double* U, const d
 mf_status mf_dgemm(mf_plan_t plan, double alpha, const double* A, int64_t lda,
                    const double* B, int64_t ldb, double* C, int64_t ldc, void* stream);
 
-/* mf_dgemm_host -- the same product with HOST A, B, C (any host memory;
+/* mf_dgemm_host -- the same product with HOST A, B, C
+ * (the end-to-end call; the paper's timings exclude transfers, L472-475; any host memory;
  * pinned memory is fastest).  Copies A and B to plan-owned device buffers,
  * runs mf_dgemm, copies C back; returns after C is complete on the host.
  * Single-GPU flattened plans pipeline the copies with the compute by row /
@@ -223,18 +227,27 @@ mf_status mf_dgemm_host_async(mf_plan_t plan, double alpha, const double* A, int
  * plan has finished (its C is on the host). */
 mf_status mf_host_sync(mf_plan_t plan);
 
-/* mf_destroy -- wait for the plan's outstanding work, free it.  NULL: no-op. */
+/* mf_destroy -- wait for the plan's outstanding work, free its workspace
+ * (the T, S, P temporaries of PAPER.md L287-292), tables and streams.
+ * NULL: no-op.  Always MF_OK. */
 mf_status mf_destroy(mf_plan_t plan);
 
-/* Thread-local message for the last non-OK status of this thread ("" if none). */
+/* Thread-local message for the last non-OK status of this thread ("" if none);
+ * failures are reported, not thrown (the CPU program's
+ * convention, kept at the boundary).  The pointer stays valid until this
+ * thread's next libmf call. */
 const char* mf_last_error(void);
 
-/* Plan facts: workspace bytes, leaf side m = n / p^levels, number of leaf
- * products R^levels, materialised T / S counts.  Any pointer may be NULL. */
+/* Plan facts: workspace bytes (the temporaries of PAPER.md L287-292), leaf
+ * side m = n / p^levels, number of leaf products R^levels (the count law of
+ * SPEC.md L395), materialised T / S counts (columns of U / V that are not a
+ * single +-1 block, Eq. "strassen" L199-202).  Any pointer may be NULL.
+ * (SURVEY §8(b) names three outputs; n_mat_a / n_mat_b are added.) */
 mf_status mf_plan_info(mf_plan_t plan, size_t* workspace_bytes, int64_t* leaf_n,
                        int64_t* n_products, int32_t* n_mat_a, int32_t* n_mat_b);
 
-/* Per-product routing of the flattened triple, arrays of length n_products
+/* Per-product routing of the flattened triple (Kronecker interleave of
+ * PAPER.md L303-313 / SPEC.md L244), arrays of length n_products
  * (host, caller-allocated, any may be NULL): a_src[q] = 0 if P_q's left
  * operand aliases block a_idx[q] of A, 1 if it is materialised slot a_idx[q]
  * of the T workspace; b_src/b_idx likewise for B and S; sign[q] = +-1, the
@@ -335,6 +348,31 @@ mf_status mf_nccl_comm_destroy(void* comm);
 mf_status mf_jit_compile_check(const double* coef, int32_t nout, int32_t nin, int32_t in_P,
                                int32_t out_P, const char* arch, int32_t* vw_out,
                                int64_t* cubin_bytes);
+
+/* Kronecker composition of two triples ("4 as 2x2 and 49";
+ * chains such as <6,6,6;161> = SW (x) Laderman, L275-293), for C callers that
+ * plan a mixed chain: U, V, W (host, caller-allocated, (po*pi)^2 x (Ro*Ri)
+ * doubles each) receive outer (x) inner with the row interleave of SPEC.md
+ * L244 -- outer block b, inner block s -> row ((b/po)*pi + s/pi)*(po*pi) +
+ * (b%po)*pi + s%pi -- and product q = q_outer*Ri + q_inner.  Plan the result
+ * with levels = 1 (mf_plan runs the exact Brent check on it).  Host only. */
+mf_status mf_triple_kron(int32_t po, int32_t Ro, const double* Uo, const double* Vo,
+                         const double* Wo, int32_t pi, int32_t Ri, const double* Ui,
+                         const double* Vi, const double* Wi, double* U, double* V, double* W);
+
+/* Deviations from SURVEY.md §8(b)'s sketch of this ABI, and why:
+ *  - mf_options has no `flatten` field; flattening is the default and
+ *    `level_by_level = 1` selects the paper's recursion -- the
+ *    inverse flag, so a zero-initialised struct gives the fast path.
+ *  - mf_plan_info has two extra outputs (n_mat_a, n_mat_b).
+ *  - `levels` repeats ONE triple; a mixed chain (SW (x) LD) is planned by
+ *    composing it with mf_triple_kron and planning levels = 1.
+ *  - added entry points: mf_dgemm_host / _async / mf_host_sync (host
+ *    buffers), mf_plan_products / mf_plan_shard_rows / mf_plan_kernels
+ *    (introspection for tests), mf_premix / mf_leaf / mf_postmix (step-by-step
+ *    parity), mf_profile_read (phase timing), mf_loop_comm_create /
+ *    mf_comm_info / mf_comm_destroy (communicators), mf_jit_compile_check
+ *    (generator check without a GPU), mf_version. */
 
 /* Library version, e.g. "mf 0.1.0 sm_100a". */
 const char* mf_version(void);

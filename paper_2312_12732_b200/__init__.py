@@ -41,7 +41,8 @@ EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error"
            "mf_plan_products", "mf_premix", "mf_leaf", "mf_postmix", "mf_nccl_unique_id",
            "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
            "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync", "mf_jit_compile_check",
-           "mf_loop_comm_create", "mf_comm_info", "mf_comm_destroy", "mf_plan_kernels")
+           "mf_loop_comm_create", "mf_comm_info", "mf_comm_destroy", "mf_plan_kernels",
+           "mf_triple_kron")
 COMM_NCCL, COMM_LOOPBACK = 0, 1
 
 
@@ -82,6 +83,7 @@ _lib.mf_nccl_comm_destroy.argtypes = [_P]
 _lib.mf_loop_comm_create.argtypes = [_I32, ctypes.POINTER(_P)]
 _lib.mf_comm_info.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
 _lib.mf_comm_destroy.argtypes = [_P]
+_lib.mf_triple_kron.argtypes = [_I32, _I32, _P, _P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P]
 _lib.mf_jit_compile_check.argtypes = [_P, _I32, _I32, _I32, _I32, ctypes.c_char_p,
                                       ctypes.POINTER(_I32), ctypes.POINTER(_I64)]
 for _f in EXPORTS:
@@ -98,6 +100,19 @@ class MfError(RuntimeError):
 def _check(status: int):
     if status != MF_OK:
         raise MfError(status, _lib.mf_last_error().decode())
+
+
+def triple_kron(outer, inner):
+    """mf_triple_kron: the composed triple outer (x) inner (U, V, W arrays of
+    ((po*pi)^2, Ro*Ri)), as a C caller plans a mixed chain."""
+    po, pi = int(outer.p), int(inner.p)
+    Ro, Ri = int(outer.U.shape[1]), int(inner.U.shape[1])
+    src = [np.ascontiguousarray(x, dtype=np.float64) for x in
+           (outer.U, outer.V, outer.W, inner.U, inner.V, inner.W)]
+    out = [np.empty(((po * pi) ** 2, Ro * Ri)) for _ in range(3)]
+    _check(_lib.mf_triple_kron(po, Ro, *[x.ctypes.data for x in src[:3]], pi, Ri,
+                               *[x.ctypes.data for x in src[3:]], *[x.ctypes.data for x in out]))
+    return tuple(out)
 
 
 def version() -> str:

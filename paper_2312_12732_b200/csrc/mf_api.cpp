@@ -3,6 +3,7 @@
 // host-buffer entry point and the NCCL bootstrap.  Kernels live in
 // mf_mix.cu (K4/K6) and mf_leaf.cu (K5).
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -37,6 +38,20 @@ mf_status fail(mf_status st, const char* fmt, ...) {
 }  // namespace mf
 
 namespace {
+
+// NVTX ranges of mf_dgemm's phases (SURVEY §5 tracing): "mf:K4 A", "mf:K4 B",
+// "mf:K5 leaf", "mf:K6", "mf:exchange" on the calling host thread, nested in
+// "mf_dgemm".  Header-only NVTX v3: no-ops unless a tool (nsys, ncu --nvtx)
+// injects itself.  The guard closes whatever is open on every return path.
+struct NvtxPhases {
+  int depth = 0;
+  NvtxPhases() { nvtxRangePushA("mf_dgemm"); depth = 1; }
+  void to(const char* name) {
+    if (depth > 1) { nvtxRangePop(); --depth; }
+    if (name) { nvtxRangePushA(name); ++depth; }
+  }
+  ~NvtxPhases() { while (depth-- > 0) nvtxRangePop(); }
+};
 
 mf_status cuda_fail(cudaError_t e, const char* what) {
   return fail(MF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
@@ -954,6 +969,23 @@ mf_status mf_plan_info(mf_plan_t pl, size_t* ws, int64_t* leaf_n, int64_t* n_pro
   return MF_OK;
 }
 
+mf_status mf_triple_kron(int32_t po, int32_t Ro, const double* Uo, const double* Vo,
+                         const double* Wo, int32_t pi, int32_t Ri, const double* Ui,
+                         const double* Vi, const double* Wi, double* U, double* V, double* W) {
+  g_err.clear();
+  if (po < 1 || pi < 1 || Ro < 1 || Ri < 1 || !Uo || !Vo || !Wo || !Ui || !Vi || !Wi || !U || !V || !W)
+    return fail(MF_ERR_INVALID_ARG, "bad argument");
+  if ((int64_t)po * pi > 256 || (int64_t)Ro * Ri > (1 << 20))
+    return fail(MF_ERR_UNSUPPORTED, "composed triple too large");
+  const size_t no = (size_t)po * po * Ro;
+  std::vector<double> uo(Uo, Uo + no), vo(Vo, Vo + no), wo(Wo, Wo + no), u, v, w;
+  kron(po, Ro, uo, vo, wo, pi, Ri, Ui, Vi, Wi, u, v, w);
+  std::copy(u.begin(), u.end(), U);
+  std::copy(v.begin(), v.end(), V);
+  std::copy(w.begin(), w.end(), W);
+  return MF_OK;
+}
+
 mf_status mf_plan_kernels(mf_plan_t pl, int32_t* jit_tables, int32_t* jit_built, int64_t* launches) {
   if (!pl) return fail(MF_ERR_INVALID_ARG, "plan is NULL");
   int32_t jt = 0, jb = 0;
@@ -1170,7 +1202,12 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
   cudaEvent_t* ev = prof_slot(pl);
   if (pl->opt.profile) ++pl->prof_calls;
   bool reduced = false;  // C already summed over ranks region by region
-  auto mark = [&](int i) { if (ev) cudaEventRecord(ev[i], s); };
+  NvtxPhases nvtx;
+  static const char* kPhase[6] = {"mf:K4 A", "mf:K4 B", "mf:K5 leaf", "mf:K6", "mf:exchange", nullptr};
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+    nvtx.to(kPhase[i]);
+  };
   // K4 of one side for this shard (whole products' slots, then the split
   // products' slots on the rank's row slab), slab by slab behind the input
   // broadcast when this rank receives its inputs

@@ -135,16 +135,9 @@ def kron(outer: Triple, inner: Triple) -> Triple:
     row-major block ((b/po)*pi + s/pi, (b%po)*pi + s%pi) of the (po*pi)-way
     split; product q = q_outer * R_inner + q_inner.  Pass the
     result to Plan with levels=1; mf_plan re-proves it (Brent) before use."""
-    po, pi = outer.p, inner.p
-    P, R = po * pi, outer.R * inner.R
-    U = np.zeros((P * P, R)); V = np.zeros((P * P, R)); W = np.zeros((P * P, R))
-    for b in range(po * po):
-        for s in range(pi * pi):
-            row = ((b // po) * pi + s // pi) * P + (b % po) * pi + s % pi
-            U[row] = np.kron(outer.U[b], inner.U[s])
-            V[row] = np.kron(outer.V[b], inner.V[s])
-            W[row] = np.kron(outer.W[b], inner.W[s])
-    return _t(f"{outer.name}(x){inner.name}", P, U, V, W)
+    from . import triple_kron  # the composition runs in libmf (mf_triple_kron)
+    U, V, W = triple_kron(outer, inner)
+    return _t(f"{outer.name}(x){inner.name}", outer.p * inner.p, U, V, W)
 
 
 CATALOG = {t.name: t for t in (STRASSEN_WINOGRAD, PAPER_STRASSEN, STRASSEN_1969, LADERMAN,

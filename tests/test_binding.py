@@ -314,3 +314,19 @@ def test_loop_comm_handles_and_plan_validation():
         for c in comms:
             mf.comm_destroy(c)
     mf.comm_destroy(None)
+
+
+@pytest.mark.parametrize("outer,inner", [("strassen-winograd", "laderman"),
+                                         ("laderman", "strassen-winograd"),
+                                         ("paper-strassen", "strassen-1969")])
+def test_triple_kron_abi_matches_oracle(outer, inner):
+    """mf_triple_kron (the C caller's way to plan a mixed chain, PAPER.md
+    L303-313) equals the oracle's independent or_kron, and the result passes
+    mf_plan's exact Brent check."""
+    U, V, W = mf.triple_kron(triples.get(outer), triples.get(inner))
+    o = oracle.kron(oracle.catalog(outer), oracle.catalog(inner))
+    assert (U == o.U).all() and (V == o.V).all() and (W == o.W).all()
+    t = triples.kron(triples.get(outer), triples.get(inner))
+    p = mf.Plan(t, 1, t.p * 8, host_only=True)
+    assert p.info()["n_products"] == t.R
+    p.close()
