@@ -2,7 +2,9 @@
 (memcheck / racecheck / synccheck, one tool per call):
 flattened + Kronecker-factored + generated + table-driven K4/K6, leaf BN=128/64
 and the simple leaf, the small-problem cluster kernel, ragged and odd sizes,
-bounded-workspace batches, host pipeline, level-by-level, sharded plans."""
+bounded-workspace batches, host pipeline, level-by-level, sharded plans, the
+ordered and bulk post-addition folds, two loopback ranks (broadcast, region
+reduce-scatter)."""
 import os
 import sys
 
@@ -53,5 +55,34 @@ for r in range(3):                        # split sharding
     with mf.Plan(T.STRASSEN_WINOGRAD, 2, n, shard_rank=r, shard_count=3) as p:
         tot += p.dgemm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
 assert (tot == (A.astype(np.int64) @ B.astype(np.int64))).all()
+run(T.STRASSEN_WINOGRAD, 2, 512, fuse_postadd=1)   # ordered fold (flags, ticket order)
+run(T.STRASSEN_WINOGRAD, 2, 400, fuse_postadd=1)   # ordered fold, ragged m=100 (scalar path)
+run(T.STRASSEN_WINOGRAD, 2, 512, fuse_postadd=2)   # bulk-reduction fold
+# two loopback ranks (threads): slab broadcasts of A, B under K4, region-wise
+# reduce-scatter of C (MF_OUT_ROWSLAB), summation kernel
+import threading  # noqa: E402
+n = 1024
+A, B = mf_inputs.pair("int8", n, 2)
+comms = mf.loop_comm_create(2)
+out = [None, None]
+
+
+def rank(r):
+    torch.cuda.set_device(0)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st), mf.Plan(T.STRASSEN_WINOGRAD, 2, n, comm=comms[r], shard_rank=r, shard_count=2,
+                                        input_mode=mf.IN_ROOT, output_mode=mf.OUT_ROWSLAB) as p:
+        C = p.dgemm(torch.from_numpy(A).cuda() if r == 0 else None,
+                    torch.from_numpy(B).cuda() if r == 0 else None, stream=st)
+        st.synchronize()
+        out[r] = C.cpu().numpy()
+
+
+th = [threading.Thread(target=rank, args=(r,)) for r in range(2)]
+[t.start() for t in th]
+[t.join() for t in th]
+for c in comms:
+    mf.comm_destroy(c)
+assert (np.concatenate(out) == (A.astype(np.int64) @ B.astype(np.int64))).all()
 torch.cuda.synchronize()
 print("sanitize smoke ok")
