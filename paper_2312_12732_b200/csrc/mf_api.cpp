@@ -443,7 +443,7 @@ mf_status run_leaf(const Plan& pl, const double* A, int64_t lda, const double* B
                            batch ? batch->n_jobs : (part ? pl.n_jobs_part : pl.n_jobs));
   LeafArgs a;
   a.A = A; a.lda = lda; a.B = B; a.ldb = ldb; a.T = T; a.S = S;
-  a.n_slots_a = pl.n_mat_a; a.n_slots_b = pl.n_mat_b;
+  a.n_slots_a = pl.n_loc_a; a.n_slots_b = pl.n_loc_b;
   a.P = pl.P; a.m = pl.m;
   a.out = out; a.ldo = ldo; a.out_block_stride = stride; a.alpha = alpha;
   a.jobs = batch ? pl.d_jobs + batch->job0 : (part ? pl.d_jobs + pl.n_jobs : pl.d_jobs);
@@ -676,9 +676,30 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     if (pl->prods[q].shard < 0) pl->my_part.push_back((int32_t)q);
   }
 
-  // plans of a compiled-in triple use the specialised K4/K6 (sharded plans:
-  // masked to their own products; slots keep the full numbering)
-  if (levels > 0 && RL <= 576 && !getenv("MF_MIX_GENERIC")) {
+  // shard-local numbering (sharded per-rank workspace ~ 1/N): a
+  // rank allocates and addresses only the T / S slots and P blocks of its own
+  // products -- whole ones, then split ones (the leaf job order) -- slots in
+  // ascending q.  The identity for unsharded plans.
+  {
+    std::vector<int32_t> jq = pl->my_prods;
+    jq.insert(jq.end(), pl->my_part.begin(), pl->my_part.end());
+    pl->loc_q.assign(RL, -1);
+    for (size_t j = 0; j < jq.size(); ++j) pl->loc_q[jq[j]] = (int32_t)j;
+    pl->n_loc_q = (int)jq.size();
+    std::sort(jq.begin(), jq.end());
+    pl->loc_a.assign(pl->n_mat_a, -1);
+    pl->loc_b.assign(pl->n_mat_b, -1);
+    for (int32_t q : jq) {
+      const Product& pr = pl->prods[q];
+      if (pr.a_src == SRC_WORKSPACE && pl->loc_a[pr.a_idx] < 0) pl->loc_a[pr.a_idx] = pl->n_loc_a++;
+      if (pr.b_src == SRC_WORKSPACE && pl->loc_b[pr.b_idx] < 0) pl->loc_b[pr.b_idx] = pl->n_loc_b++;
+    }
+  }
+
+  // plans of a compiled-in triple use the specialised K4/K6 (their slot and
+  // product numbering is the whole triple's: unsharded plans only; a shard's
+  // K4 / K6 are generated over its own slots and products)
+  if (levels > 0 && RL <= 576 && shard_count == 1 && !getenv("MF_MIX_GENERIC")) {
     pl->fixed_id = fixed_match(*pl);
     if (pl->fixed_id == 0) pl->fixed_id = kron_match(*pl);
   }
@@ -698,20 +719,23 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       const Product& pr = pl->prods[q];
       if ((side == 0 ? pr.a_src : pr.b_src) != SRC_WORKSPACE) continue;
       for (int k = 0; k < NB; ++k) t.coef.push_back(M[k * RL + q]);
-      t.out_map.push_back(side == 0 ? pr.a_idx : pr.b_idx);
+      t.out_map.push_back(side == 0 ? pl->loc_a[pr.a_idx] : pl->loc_b[pr.b_idx]);
       ++t.nout;
     }
   };
+  // K6 over the shard's P blocks (local product index = input index)
   auto post_table = [&](MixTable& c, bool with_part) {
-    c.nin = (int)RL;
+    const int nq = pl->n_loc_q;
+    c.nin = nq;
     c.nout = NB;
-    c.coef.assign((size_t)NB * RL, 0.0);
+    c.coef.assign((size_t)NB * nq, 0.0);
     for (int i = 0; i < NB; ++i) c.out_map.push_back(i);
     for (int32_t q : pl->my_prods)
-      for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+      for (int i = 0; i < NB; ++i) c.coef[(size_t)i * nq + pl->loc_q[q]] = pl->W[i * RL + q] * pl->prods[q].sign;
     if (with_part)
       for (int32_t q : pl->my_part)
-        for (int i = 0; i < NB; ++i) c.coef[i * RL + q] = pl->W[i * RL + q] * pl->prods[q].sign;
+        for (int i = 0; i < NB; ++i)
+          c.coef[(size_t)i * nq + pl->loc_q[q]] = pl->W[i * RL + q] * pl->prods[q].sign;
   };
   if (levels > 0) {
     std::vector<int32_t> all = pl->my_prods;
@@ -775,8 +799,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   // ---- device allocations ----
   const int64_t mm = pl->m * pl->m;
   if (levels > 0) {
-    size_t tb = sizeof(double) * mm * pl->n_mat_a, sb = sizeof(double) * mm * pl->n_mat_b,
-           pb = sizeof(double) * mm * RL;
+    size_t tb = sizeof(double) * mm * pl->n_loc_a, sb = sizeof(double) * mm * pl->n_loc_b,
+           pb = sizeof(double) * mm * pl->n_loc_q;
     if (!pl->batches.empty()) {
       int na = 0, nb = 0, np = 0;
       for (auto& b : pl->batches) {
@@ -816,13 +840,9 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
     // generate and compile their kernels now (mf_jit.cpp)
     std::vector<JitJob> jj;
     if (pl->fixed_id == 0 && levels > 0) {
+      // (a shard's K4 reads just the input blocks its slots use)
       for (MixTable* t : {&pl->mixA, &pl->mixA2, &pl->mixB}) jj.push_back({t, pl->P, 0});
       for (MixTable* t : {&pl->mixC, &pl->mixC2}) jj.push_back({t, 0, pl->P});
-    } else if (levels > 0 && pl->fixed_id < 8 && shard_count > 1 && !getenv("MF_SHARD_MASKED")) {
-      // a shard's K4 over its own slots only: the generated kernel reads just
-      // the input blocks those slots use (the masked compiled-in kernel
-      // streams all of them); same flat ascending order, so bitwise the same
-      for (MixTable* t : {&pl->mixA, &pl->mixA2, &pl->mixB}) jj.push_back({t, pl->P, 0});
     }
     for (auto& b : pl->batches) {
       jj.push_back({&b.mixA, pl->P, 0});
@@ -838,10 +858,10 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   for (int32_t q : job_q) {
     const Product& pr = pl->prods[q];
     LeafJob j;
-    j.a_coord = pr.a_src == SRC_INPUT ? ((pr.a_idx / pl->P) << 16) | (pr.a_idx % pl->P) : pr.a_idx;
-    j.b_coord = pr.b_src == SRC_INPUT ? ((pr.b_idx / pl->P) << 16) | (pr.b_idx % pl->P) : pr.b_idx;
+    j.a_coord = pr.a_src == SRC_INPUT ? ((pr.a_idx / pl->P) << 16) | (pr.a_idx % pl->P) : pl->loc_a[pr.a_idx];
+    j.b_coord = pr.b_src == SRC_INPUT ? ((pr.b_idx / pl->P) << 16) | (pr.b_idx % pl->P) : pl->loc_b[pr.b_idx];
     j.flags = (pr.a_src == SRC_WORKSPACE ? 1 : 0) | (pr.b_src == SRC_WORKSPACE ? 2 : 0);
-    j.out_idx = levels > 0 ? q : 0;
+    j.out_idx = levels > 0 ? pl->loc_q[q] : 0;
     jobs.push_back(j);
   }
   pl->n_jobs = (int)pl->my_prods.size();
@@ -880,7 +900,9 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
   if (pl->fuse) {
     // fused post-addition: product q feeds C block i with W'[i][q] (alias sign
     // folded in); terms sorted by coefficient so each value is staged once
-    std::vector<int32_t> off(RL + 1, 0);
+    // indexed by the local product index (the leaf job's out_idx)
+    const int nq = pl->n_loc_q;
+    std::vector<int32_t> off(nq + 1, 0);
     std::vector<PostTerm> terms;
     std::vector<char> mine(RL, 0);
     for (int32_t q : job_q) mine[q] = 1;
@@ -899,23 +921,27 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
         return fail(MF_ERR_BAD_TRIPLE, "C block %d has no product (ordered fold)", i);
       }
     std::vector<int32_t> n_seen(NB, 0);
+    std::vector<std::vector<PostTerm>> per(nq);
     for (int64_t q = 0; q < RL; ++q) {
-      off[q] = (int32_t)terms.size();
       if (!mine[q]) continue;
-      const size_t first = terms.size();
+      std::vector<PostTerm>& tq = per[pl->loc_q[q]];
       for (int i = 0; i < NB; ++i) {
         const double w = pl->W[i * RL + q] * pl->prods[q].sign;
         if (w == 0.0) continue;
         const int32_t fl = (q == q_first[i] ? POST_FIRST : 0) | (q == q_last[i] ? POST_LAST : 0) |
                            (n_seen[i]++ << 8);  // ordered fold: the product's rank in block i
-        terms.push_back(PostTerm{(int32_t)(((i / pl->P) << 16) | (i % pl->P)), fl, w});
+        tq.push_back(PostTerm{(int32_t)(((i / pl->P) << 16) | (i % pl->P)), fl, w});
       }
       // the bulk-reduction fold restages its tile once per coefficient value
       if (!pl->fuse_ordered)
-        std::stable_sort(terms.begin() + first, terms.end(),
+        std::stable_sort(tq.begin(), tq.end(),
                          [](const PostTerm& x, const PostTerm& y) { return x.coef < y.coef; });
     }
-    off[RL] = (int32_t)terms.size();
+    for (int j = 0; j < nq; ++j) {
+      off[j] = (int32_t)terms.size();
+      terms.insert(terms.end(), per[j].begin(), per[j].end());
+    }
+    off[nq] = (int32_t)terms.size();
     if (pl->fuse_ordered) {
       // per-tile-position flags of the widest tiling (64-wide tiles), then the
       // ticket and done counters; zero between launches
@@ -1302,15 +1328,15 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
       for (int32_t q : pl->my_prods) {
         const Product& pr = pl->prods[q];
         const double* X = pr.a_src == SRC_WORKSPACE
-                              ? pl->T + (int64_t)pr.a_idx * mm
+                              ? pl->T + (int64_t)pl->loc_a[pr.a_idx] * mm
                               : A + (int64_t)(pr.a_idx / pl->P) * m * lda + (pr.a_idx % pl->P) * m;
         const double* Y = pr.b_src == SRC_WORKSPACE
-                              ? pl->S + (int64_t)pr.b_idx * mm
+                              ? pl->S + (int64_t)pl->loc_b[pr.b_idx] * mm
                               : B + (int64_t)(pr.b_idx / pl->P) * m * ldb + (pr.b_idx % pl->P) * m;
         const int64_t ldx = pr.a_src == SRC_WORKSPACE ? m : lda;
         const int64_t ldy = pr.b_src == SRC_WORKSPACE ? m : ldb;
         if ((st = mf_dgemm(static_cast<mf_plan_t>(pl->child), 1.0, X, ldx, Y, ldy,
-                           pl->Pw + (int64_t)q * mm, m, stream)) != MF_OK)
+                           pl->Pw + (int64_t)pl->loc_q[q] * mm, m, stream)) != MF_OK)
           return st;
       }
     } else if (comm_regions(*pl) > 1) {

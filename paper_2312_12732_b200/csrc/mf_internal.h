@@ -174,6 +174,10 @@ struct Plan {
   std::vector<int32_t> my_prods;  // whole products q
   std::vector<int32_t> my_part;   // split products q (this rank: rows part_rows)
   int64_t part_r0 = 0, part_r1 = 0;
+  // shard-local numbering: global slot / product -> local index (-1: not this
+  // rank's), and the local counts the workspace is sized by
+  std::vector<int32_t> loc_a, loc_b, loc_q;
+  int n_loc_a = 0, n_loc_b = 0, n_loc_q = 0;
   MixTable mixA, mixB;            // pre-additions: A slots of whole products, all B slots used
   MixTable mixA2;                 // A slots of split products (rows part_rows only)
   MixTable mixC;                  // post-addition over the whole products (zero coef elsewhere)

@@ -491,6 +491,25 @@ def test_split_sharding_partials_sum_to_product(N):
     assert scaled(host(total), ref, A, B) <= 2e-13
 
 
+@pytest.mark.parametrize("N", [2, 3, 8])
+def test_sharded_workspace_shrinks_with_ranks(N):
+    """A shard allocates only its own products' T / S slots and P blocks
+    (shard-local numbering): per-rank workspace ~ 1/N of the 1-GPU plan's
+    (SW^2 n = 4096: 129 blocks of 8 MB on one GPU; rank r of 8 holds at most
+    7 products, <= 21 blocks)."""
+    n = 4096
+    with mf.Plan(triples.get(SW), 2, n) as p:
+        full = p.info()["workspace_bytes"]
+    blk = 8 * (n // 4) ** 2
+    assert full == 129 * blk
+    for r in range(N):
+        with mf.Plan(triples.get(SW), 2, n, shard_rank=r, shard_count=N) as p:
+            ws = p.info()["workspace_bytes"]
+            mine = int((p.products()["shard"] == r).sum() + (p.products()["shard"] == -1).sum())
+            assert ws <= 3 * mine * blk
+            assert ws <= (1.0 / N + 0.2) * full
+
+
 def test_nccl_single_rank_plan_matches_local():
     """The NCCL exchange step of the sharded path (mf_nccl_unique_id /
     mf_nccl_comm_create / reduce of C in mf_dgemm) on a 1-rank communicator:

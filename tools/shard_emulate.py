@@ -1,8 +1,12 @@
 """Emulated product sharding on one GPU: every rank r of N runs its own plan
 (shard_rank = r, shard_count = N, no communicator: the plan computes rank r's
 partial C with the real kernels), timed with CUDA events.  max over ranks of
-the per-rank step time = the compute part of an N-GPU step; the NCCL reduce of
-C (overlapped region by region in the real run) is not included.
+the per-rank step time = the compute part of an N-GPU step; the exchange (the
+MF_IN_ROOT slab broadcasts of A and B and the reduce of C, overlapped region
+by region in the real run) is NOT included -- its volumes per rank are
+reported, not timed (one GPU has no NVLink peer).  SM clocks and throttle
+reasons are sampled over the whole run (bench.Clocks).  Emulation, not a
+multi-GPU measurement.
 
     python tools/shard_emulate.py [--n 16384] [--Ns 2,4,8]
 """
@@ -41,6 +45,9 @@ def main():
     ap.add_argument("--regions", type=int, default=0,
                     help="comm_regions of the real multi-GPU run (8 by default there); 0 = one launch")
     a = ap.parse_args()
+    from bench import Clocks
+    clocks = Clocks(0)
+    clocks.start()
     n = a.n
     A, B = mf_inputs.device_pair("uniform", n, 0, device="cuda:0")
     C = torch.empty_like(A)
@@ -57,9 +64,14 @@ def main():
                 per.append(step_ms(p, A, B, C))
             torch.cuda.empty_cache()
         tmax = max(per)
+        mat = 8.0 * n * n
         print(json.dumps({"n": n, "N": N, "regions": a.regions, "rank_ms": [round(x, 3) for x in per], "max_ms": tmax,
                           "tflops_compute_only": fl / tmax / 1e9,
-                          "efficiency_vs_1gpu": t1 / (N * tmax)}), flush=True)
+                          "efficiency_vs_1gpu": t1 / (N * tmax),
+                          "exchange_bytes_per_step": {"broadcast_A_B_from_root": 2 * mat,
+                                                      "reduce_C_to_root": mat},
+                          "timed": "compute only (every rank's real kernels, max over ranks)"}), flush=True)
+    print(json.dumps({"clocks": clocks.stop()}), flush=True)
 
 
 if __name__ == "__main__":
