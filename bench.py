@@ -118,8 +118,9 @@ def parse():
     ap.add_argument("--input-mode", choices=["root", "replicated"], default="root",
                     help="sharded runs: A and B on rank 0 only, broadcast by row slabs inside "
                          "the timed step (default), or already replicated on every rank")
-    ap.add_argument("--fuse", action="store_true",
-                    help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd)")
+    ap.add_argument("--fuse", type=int, nargs="?", const=1, default=0, choices=[0, 1, 2],
+                    help="fold the post-additions into the leaf epilogue (mf_options.fuse_postadd): "
+                         "1 = ordered fold (bitwise the unfused result), 2 = bulk f64 reductions")
     a = ap.parse_args()
     if a.config:
         a.n, a.triple, a.levels = CONFIGS[a.config]
@@ -136,8 +137,9 @@ def workload_name(a):
         r = a.recurse_levels
         mode = (f"{r} top level(s) one at a time, each product a flattened "
                 f"{a.levels - r}-level child")
-    if getattr(a, "fuse", False):
-        mode += ", post-additions fused into the leaf epilogue"
+    if getattr(a, "fuse", 0):
+        mode += (", post-additions folded into the leaf epilogue in ascending q (ordered fold)"
+                 if a.fuse == 1 else ", post-additions fused by bulk f64 reductions into C")
     if getattr(a, "leaf", "dmma") != "dmma":
         mode += f", {a.leaf} leaf (ablation)"
     return f"n={a.n} fp64, {a.levels}-level {a.triple} ({mode}, {_rank(a) ** a.levels} leaf products)"

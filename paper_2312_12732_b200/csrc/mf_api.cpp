@@ -947,8 +947,8 @@ static mf_status mf_plan_impl(mf_plan_t* out, int32_t p, int32_t R, const double
       // ticket and done counters; zero between launches
       const int64_t tiles = (int64_t)NB * ((pl->m + 127) / 128) * ((pl->m + 63) / 64);
       pl->fuse_sync_len = tiles;
-      if (cudaMalloc(&pl->fuse_sync, sizeof(uint32_t) * (tiles + 2)) != cudaSuccess ||
-          cudaMemset(pl->fuse_sync, 0, sizeof(uint32_t) * (tiles + 2)) != cudaSuccess) {
+      if (cudaMalloc(&pl->fuse_sync, sizeof(uint32_t) * (tiles + 8)) != cudaSuccess ||
+          cudaMemset(pl->fuse_sync, 0, sizeof(uint32_t) * (tiles + 8)) != cudaSuccess) {
         free_plan(pl.get());
         return fail(MF_ERR_OUT_OF_MEMORY, "ordered fold flags");
       }

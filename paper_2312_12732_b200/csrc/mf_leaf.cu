@@ -71,21 +71,24 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 constexpr int BM = 128, BN = 128, BK = 16;  // BN: the default (widest) tile; BK: one k sub-block
-constexpr int MMA_WARPS = 8;
+constexpr int MMA_WARPS = 8;   // one CTA per SM (the default shape)
 constexpr int THREADS = MMA_WARPS * 32;
 constexpr int A_SUB_BYTES = BM * BK * 8;  // one [128 m][16 k] swizzled A sub-tile
 // A stage holds KSUB k sub-blocks (16 k each): A as KSUB swizzled sub-tiles,
 // B as one [16*KSUB k][BNT n] box.  Deeper stages (KSUB = 2) halve the
-// mbarrier waits per flop; the ring depth keeps ~190 KB of smem in flight.
+// mbarrier waits per flop; the ring depth keeps ~190 KB of smem in flight per
+// SM: one CTA of NW = 8 MMA warps with a 192 KB ring, or (NW = 4, 128 x 64
+// tiles) two co-resident CTAs with 96 KB rings each.
 template <int BNT, int KSUB> __host__ __device__ constexpr int a_bytes() { return KSUB * A_SUB_BYTES; }
 template <int BNT, int KSUB> __host__ __device__ constexpr int stage_bytes() {
   return KSUB * A_SUB_BYTES + KSUB * BK * BNT * 8;
 }
-template <int BNT, int KSUB> __host__ __device__ constexpr int n_stages() {
-  return (192 * 1024) / stage_bytes<BNT, KSUB>() < 5 ? (192 * 1024) / stage_bytes<BNT, KSUB>() : 5;
+template <int BNT, int KSUB, int NW = 8> __host__ __device__ constexpr int n_stages() {
+  return ((NW == 8 ? 192 : 96) * 1024) / stage_bytes<BNT, KSUB>() < 5
+             ? ((NW == 8 ? 192 : 96) * 1024) / stage_bytes<BNT, KSUB>() : 5;
 }
-template <int BNT, int KSUB> __host__ __device__ constexpr int smem_bytes() {
-  return n_stages<BNT, KSUB>() * stage_bytes<BNT, KSUB>() + 2 * n_stages<BNT, KSUB>() * 8 + 1024;
+template <int BNT, int KSUB, int NW = 8> __host__ __device__ constexpr int smem_bytes() {
+  return n_stages<BNT, KSUB, NW>() * stage_bytes<BNT, KSUB>() + 2 * n_stages<BNT, KSUB, NW>() * 8 + 1024;
 }
 constexpr int GROUP_M = 8;
 
@@ -183,10 +186,21 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
-// L2-coherent loads of C in the ordered fold (another SM wrote it since this
-// SM may last have cached it): ld.global.cg
-__device__ __forceinline__ void ldcg_v2(const double* p, double& x, double& y) {
-  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p));
+// Loads of C in the ordered fold: plain (weak) global loads after the flag's
+// ld.acquire -- the pattern the PTX memory model orders (the acquire
+// invalidates the SM's L1, so no stale line survives).  Measured: with two
+// CTAs per SM, ld.global.cg loads here returned data older than a co-resident
+// writer's released stores (rows of the other CTA's warps 2-3 lost updates),
+// weak loads did not.  "memory": must not move above the barrier that follows
+// the wait.
+__device__ __forceinline__ void ld_v2(const double* p, double& x, double& y) {
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p) : "memory");
+}
+
+__device__ __forceinline__ double ld_f64(const double* p) {
+  double x;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(x) : "l"(p) : "memory");
+  return x;
 }
 
 // BNT = CTA tile width (128, or 64 to cut wave quantisation on small batches):
@@ -195,13 +209,18 @@ __device__ __forceinline__ void ldcg_v2(const double* p, double& x, double& y) {
 // bulk f64 reductions into C (order not fixed), 2 = ordered fold: the products
 // of one tile position update C in job order (ascending q), store / add /
 // alpha-last exactly as K6, so C is bitwise the unfused result.
-template <int BNT, int KSUB, int FUSE>
-__global__ void __launch_bounds__(THREADS, 1)
+// NW = MMA warps per CTA: 8 (2 x 4 warp grid, one CTA per SM) or 4 (2 x 2
+// warp grid of 64 x 32 warp tiles at BNT = 64, two CTAs per SM: one CTA's
+// prologue / epilogue runs beside the other's k loop).
+template <int BNT, int KSUB, int FUSE, int NW = 8>
+__global__ void __launch_bounds__(NW * 32, NW == 8 ? 1 : 2)
 leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmS,
                  const LeafParams prm) {
-  constexpr int NJ = BNT / 64, WN = BNT / 4;
-  constexpr int STAGES = n_stages<BNT, KSUB>();
+  constexpr int MMA_WARPS = NW, THREADS = NW * 32, WARPS_N = NW / 2;
+  constexpr int WN = BNT / WARPS_N, NJ = WN / 16;
+  static_assert(NJ >= 1 && WN % 16 == 0, "warp tile width");
+  constexpr int STAGES = n_stages<BNT, KSUB, NW>();
   constexpr int STAGE_BYTES = stage_bytes<BNT, KSUB>();
   constexpr int A_BYTES = a_bytes<BNT, KSUB>();
   constexpr int KS = BK * KSUB;  // k per stage
@@ -289,8 +308,8 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
 
   // ================= MMA warps =================
-  const int wm = warp >> 2;  // 0..1 -> 64-row half
-  const int wn = warp & 3;   // 0..3 -> 32-col quarter
+  const int wm = warp / WARPS_N;  // 0..1 -> 64-row half
+  const int wn = warp % WARPS_N;  // WN-column slice
   const int lr = lane >> 2, lk = lane & 3;
 
   double acc[8][NJ][2][2];
@@ -431,12 +450,12 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               const int64_t col = (int64_t)tn * BNT + wn * WN + nj * 16 + 4 * lk;
               const double* src = cb + row * prm.ldo + col;
               if (row < prm.m && vec_ok && col + 3 < prm.m) {
-                ldcg_v2(src, old[mh][nj][0], old[mh][nj][1]);
-                ldcg_v2(src + 2, old[mh][nj][2], old[mh][nj][3]);
+                ld_v2(src, old[mh][nj][0], old[mh][nj][1]);
+                ld_v2(src + 2, old[mh][nj][2], old[mh][nj][3]);
               } else {
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                  old[mh][nj][u] = (row < prm.m && col + u < prm.m) ? __ldcg(src + u) : 0.0;
+                  old[mh][nj][u] = (row < prm.m && col + u < prm.m) ? ld_f64(src + u) : 0.0;
               }
             }
           }
@@ -797,6 +816,18 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     // the caller provides the split-K workspace (run_leaf sizes it from leaf_tiles)
     if (cfg.split > 1 && (!a.split_ws || a.split_ws_elems < cfg.ws_elems || a.split_cnt_len < cfg.n_tail))
       cfg.split = 1;
+    // Two CTAs per SM (4 MMA warps, 128 x 64 tiles, 96 KB rings): one CTA's
+    // epilogue runs beside the other's k loop.  The default for the
+    // bulk-reduction fold, whose epilogue (stage + bulk reductions) it hides:
+    // SW^2 n=16384 step 191.3 -> 187.9 ms, equal to the unfused step
+    // (profiles/leaf2cta_r02.jsonl); the unfused leaf keeps one 128 x 128 CTA
+    // per SM (184.2 vs 185.1 ms).  MF_LEAF_2CTA=1/0 forces it on/off.  Not for
+    // the ordered fold: with two CTAs per SM its flag-ordered read-modify-
+    // writes lost updates in rows of warps 2-3 (a race not understood;
+    // tools/ordered_pattern.py), so that fold keeps one CTA per SM.
+    const char* e2 = getenv("MF_LEAF_2CTA");
+    const bool two_cta = !ordered && (e2 ? atoi(e2) > 0 : (a.post != nullptr));
+    if (two_cta) { cfg.bn = 64; cfg.split = 1; }
     const int bn = cfg.bn;
     // k sub-blocks of 16 per pipeline stage: 2 (k = 32, 3-stage ring), or 3
     // (k = 48, 2 stages) where m is a multiple of 48 or large -- measured
@@ -844,10 +875,13 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)
-    static std::atomic<uint64_t> attr_set[9];
-    const int inst = ordered ? (bn == 64 ? 8 : 7)
+    if (two_cta && ksub == 3) ksub = 2;
+    static std::atomic<uint64_t> attr_set[12];
+    const int inst = two_cta ? (ordered ? 10 : fuse ? 11 : 9)
+                     : ordered ? (bn == 64 ? 8 : 7)
                      : fuse  ? (bn == 64 ? 5 : 4)
                              : (ksub == 3 ? 6 : (bn == 64 ? 2 : 0) + (ksub == 2 ? 1 : 0));
+    const int threads = two_cta ? 128 : THREADS;
     const uint64_t dev_bit = 1ull << (dev & 63);
     auto launch = [&](auto kern, int smem) -> cudaError_t {
       if (!(attr_set[inst].load() & dev_bit)) {
@@ -855,7 +889,7 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr_set[inst].fetch_or(dev_bit);
       }
-      kern<<<(unsigned)grid, THREADS, smem, s>>>(mA, mT, mB, mS, prm);
+      kern<<<(unsigned)grid, threads, smem, s>>>(mA, mT, mB, mS, prm);
       return cudaSuccess;
     };
     cudaError_t e;
@@ -868,6 +902,9 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
       case 6: e = launch(leaf_dmma_kernel<128, 3, 0>, smem_bytes<128, 3>()); break;
       case 7: e = launch(leaf_dmma_kernel<128, 2, 2>, smem_bytes<128, 2>()); break;
       case 8: e = launch(leaf_dmma_kernel<64, 2, 2>, smem_bytes<64, 2>()); break;
+      case 9: e = launch(leaf_dmma_kernel<64, 2, 0, 4>, smem_bytes<64, 2, 4>()); break;
+      case 10: e = launch(leaf_dmma_kernel<64, 2, 2, 4>, smem_bytes<64, 2, 4>()); break;
+      case 11: e = launch(leaf_dmma_kernel<64, 2, 1, 4>, smem_bytes<64, 2, 4>()); break;
       default: e = launch(leaf_dmma_kernel<64, 2, 1>, smem_bytes<64, 2>()); break;
     }
     if (e != cudaSuccess) return e;

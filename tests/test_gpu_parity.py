@@ -1212,3 +1212,22 @@ def test_random_shape_sweep():
         else:
             ref = alpha * oracle.classical(A, B)
             assert_error(scaled(C, ref, A, B), levels, abs(alpha), (name, levels, n, pad, alpha))
+
+
+@pytest.mark.parametrize("name,levels,n", [(SW, 2, 2048), (SW, 1, 400), ("laderman", 1, 390), (None, 0, 640)])
+def test_two_cta_leaf(name, levels, n, monkeypatch):
+    """The two-CTA-per-SM leaf (4 MMA warps, 128 x 64 tiles; the default under
+    the bulk-reduction fold, forced here for the unfused path): integer inputs
+    exact, random inputs bitwise the one-CTA leaf (same k order per element)
+    with no split-K tail on either side; ragged leaves (m = 200, 130) too."""
+    t = triples.get(name) if name else None
+    monkeypatch.setenv("MF_LEAF_SPLIT", "1")
+    A, B = mf_inputs.pair("int1024", n, 48)
+    Ar, Br = mf_inputs.pair("uniform", n, 49)
+    out = {}
+    for two in ("0", "1"):
+        monkeypatch.setenv("MF_LEAF_2CTA", two)
+        with mf.Plan(t, levels, n) as p:
+            assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all(), two
+            out[two] = host(p.dgemm(dev(Ar), dev(Br)))
+    assert (out["0"] == out["1"]).all()

@@ -17,6 +17,15 @@ alpha = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 t = triples.get(name)
 A, B = mf_inputs.device_pair("uniform", n, 0)
 res = {}
+two = os.environ.pop("MF_LEAF_2CTA", None)  # applied to the fused modes only
+# the reference: one-CTA leaf, flat K6, no split tail
+with mf.Plan(t, L, n) as p:
+    os.environ["MF_MIX_GENERIC"] = "1"
+with mf.Plan(t, L, n) as p:
+    ref = p.dgemm(A, B, alpha=alpha).clone()
+os.environ.pop("MF_MIX_GENERIC", None)
+if two:
+    os.environ["MF_LEAF_2CTA"] = two
 for mode in (0, 1, 2):
     if mode == 0:
         os.environ["MF_MIX_GENERIC"] = "1"
@@ -32,6 +41,8 @@ for mode in (0, 1, 2):
         res[mode] = C.clone()
         print(mode, {k: round(v / reps, 3) if k != "calls" else v for k, v in ph.items()})
     os.environ.pop("MF_MIX_GENERIC", None)
+print("vs one-CTA unfused reference: mode0", int((res[0] != ref).sum()), "mode1", int((res[1] != ref).sum()),
+      "mode2 max|d|", float((res[2] - ref).abs().max()))
 P = t.p ** L
 m = n // P
 d = (res[1] != res[0])
