@@ -1126,6 +1126,11 @@ static mf_status ensure_events(std::vector<cudaEvent_t>& v, size_t k) {
   return MF_OK;
 }
 
+// the default flattened schedule (not level-by-level, fused or batched)
+static bool levels_flat(const Plan& pl) {
+  return pl.levels > 0 && !pl.child && !pl.fuse && pl.batches.empty();
+}
+
 // Input row slabs of the MF_IN_ROOT broadcast (and of the K4 launches that
 // follow each slab): as many as the exchange regions, at least 1.
 static int input_slabs(const Plan& pl) {
@@ -1199,7 +1204,9 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     // the previous call's reads of the replicas)
     MF_CUDA(cudaEventRecord(pl->in_events[2 * KI + 1], s), "event");
     MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->in_events[2 * KI + 1], 0), "wait");
-    for (int side = 0; side < 2; ++side) {
+    // B first: every product needs all of S_q, while the leaf's row region k
+    // needs only A's slab k -- so region k can start when A's slab k landed
+    for (int side = 1; side >= 0; --side) {
       double* buf = side == 0 ? bufA : bufB;
       for (int k = 0; k < KI; ++k) {
         const auto sr = tile_piece(m, k, KI);
@@ -1234,6 +1241,21 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     if (ev) cudaEventRecord(ev[i], s);
     nvtx.to(kPhase[i]);
   };
+  // K4(A) on rows r of every block: the whole products' slots, then the split
+  // products' slots on the part of r inside the rank's row slab
+  auto premix_a_rows = [&](Rows r) -> mf_status {
+    MF_CUDA(launch_premix(*pl, pl->mixA, A, lda, pl->T, s, r), "pre-add A (K4)");
+    if (!pl->my_part.empty()) {
+      Rows pr;
+      pr.r0 = std::max<int64_t>(r.r0, pl->part_r0);
+      pr.r1 = std::min<int64_t>(r.end(m), pl->part_r1);
+      if (pr.r0 < pr.r1) MF_CUDA(launch_premix(*pl, pl->mixA2, A, lda, pl->T, s, pr), "pre-add A (K4, split)");
+    }
+    return MF_OK;
+  };
+  // MF_IN_ROOT with the region schedule: K4(A) of slab k runs right before the
+  // leaf's region k (same rows), so A's broadcast overlaps the leaf, not only K4
+  const bool a_by_region = wait_inputs && levels_flat(*pl) && comm_regions(*pl) == KI && KI > 1;
   // K4 of one side for this shard (whole products' slots, then the split
   // products' slots on the rank's row slab), slab by slab behind the input
   // broadcast when this rank receives its inputs
@@ -1251,13 +1273,10 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
         r.r0 = sr.first; r.r1 = sr.second;
         if (r.r1 <= r.r0) continue;
       }
-      MF_CUDA(launch_premix(*pl, whole, X, ldx, out, s, r), side == 0 ? "pre-add A (K4)" : "pre-add B (K4)");
-      if (side == 0 && !pl->my_part.empty()) {
-        Rows pr;
-        pr.r0 = std::max<int64_t>(r.r0, pl->part_r0);
-        pr.r1 = std::min<int64_t>(r.end(m), pl->part_r1);
-        if (pr.r0 < pr.r1)
-          MF_CUDA(launch_premix(*pl, pl->mixA2, X, ldx, out, s, pr), "pre-add A (K4, split)");
+      if (side == 0) {
+        if ((st = premix_a_rows(r)) != MF_OK) return st;
+      } else {
+        MF_CUDA(launch_premix(*pl, whole, X, ldx, out, s, r), "pre-add B (K4)");
       }
     }
     return MF_OK;
@@ -1315,12 +1334,13 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     mark(3);
   } else {
     // a1, a2: fused pre-additions (K4) for this shard's materialised operands
-    if ((st = premix_side(0)) != MF_OK) return st;
+    // (a_by_region: K4(A) runs per region below -- profiled in the leaf phase)
+    if (!a_by_region && (st = premix_side(0)) != MF_OK) return st;
     mark(1);
     if ((st = premix_side(1)) != MF_OK) return st;
     mark(2);
     // aliased operands are read by the leaf straight from the received inputs
-    if (wait_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
+    if (wait_inputs && !a_by_region) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
     if (pl->child) {
       // a5: level by level -- each product P_q' = X_q Y_q is itself computed by
       // the (levels-1)-level child plan ("recursively solve P_i")
@@ -1366,6 +1386,10 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
         if (rg.second <= rg.first) continue;
         Rows r;
         r.r0 = rg.first; r.r1 = rg.second;
+        if (a_by_region) {  // A's slab k (= region k's rows) landed: its K4, then the leaf
+          MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[k], 0), "wait");
+          if ((st = premix_a_rows(r)) != MF_OK) return st;
+        }
         if ((st = run_leaf(*pl, A, lda, B, ldb, pl->T, pl->S, pl->Pw, m, m * m, 1.0, s, r)) != MF_OK)
           return st;
         if (!pl->my_part.empty()) {
