@@ -16,7 +16,9 @@
 // by integer exactness and the error bound).
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "mf_internal.h"
 
@@ -26,6 +28,21 @@ namespace mf {
 namespace {
 
 constexpr int TINY_THREADS = 256;
+
+#ifdef MF_TINY_TRACE
+// diagnostic build only (-DMF_TINY_TRACE): globaltimer stamps of CTA c's thread 0
+__device__ unsigned long long g_tiny_trace[8][12];
+__device__ __forceinline__ void tstamp(int i) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_tiny_trace[blockIdx.x & 7][i] = t;
+  }
+}
+#define TSTAMP(i) tstamp(i)
+#else
+#define TSTAMP(i)
+#endif
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,6 +77,7 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
   double* sAll = sP + per * up(mm);     // every product, gathered for the post-addition
   const int mmp = up(mm);               // product stride in sP / sAll
 
+  TSTAMP(0);
   __shared__ __align__(8) uint64_t s_bar;  // gathered products landed
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&s_bar)) : "memory");
@@ -92,6 +110,7 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
     }
   }
   __syncthreads();
+  TSTAMP(1);
   for (int q = me, j = 0; q < R; q += cs, ++j) {
     // T_q, S_q: block k of X is rows (k/P)*m.., cols (k%P)*m..
     for (int e = threadIdx.x; e < mm; e += blockDim.x) {
@@ -108,6 +127,7 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
       sS[e] = s;
     }
     __syncthreads();
+    if (j == 0) TSTAMP(2);
     double* Pq = sP + (size_t)j * mmp;
     if (!(m & 7)) {
       // P_q = T_q S_q on the FP64 tensor path: 8x8 tiles over the warps,
@@ -150,7 +170,9 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
     }
     __syncthreads();
   }
+  TSTAMP(3);
   cluster.sync();  // every CTA's products are complete and every barrier initialised
+  TSTAMP(4);
   const uint32_t bytes = (uint32_t)mm * 8;
   if (!(bytes & 15)) {
     // push: thread d sends this CTA's products to CTA d's gather area with
@@ -181,7 +203,9 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
       for (int e = threadIdx.x; e < mm; e += blockDim.x) sAll[(size_t)q * mmp + e] = src[e];
     }
   }
+  TSTAMP(5);
   cluster.sync();  // no CTA leaves while another may still read its products
+  TSTAMP(6);
   // C: element (i, r, c) of block i, ascending q (K6's order), alpha last
   const int tid = me * blockDim.x + threadIdx.x, nth = cs * blockDim.x;
   for (int e = tid; e < NB * mm; e += nth) {
@@ -195,9 +219,16 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
     const int r = rc / m, c = rc - r * m;
     C[(int64_t)((i / P) * m + r) * ldc + (i % P) * m + c] = acc;
   }
+  TSTAMP(7);
 }
 
 }  // namespace
+
+#ifdef MF_TINY_TRACE
+extern "C" int mf_debug_tiny_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_tiny_trace, sizeof(unsigned long long) * 8 * 12);
+}
+#endif
 
 size_t tiny_smem(const Plan& pl);
 
@@ -207,8 +238,14 @@ bool tiny_eligible(const Plan& pl) {
          pl.d_tinyU != nullptr && tiny_smem(pl) <= 200 * 1024;
 }
 
+static int tiny_cluster(const Plan& pl) {
+  int cs = (int)std::min<int64_t>(8, pl.RL);
+  if (const char* e = getenv("MF_TINY_CS")) cs = std::max(1, std::min(cs, atoi(e)));  // experiment
+  return cs;
+}
+
 size_t tiny_smem(const Plan& pl) {
-  const int cs = (int)std::min<int64_t>(8, pl.RL);
+  const int cs = tiny_cluster(pl);
   auto up = [](int64_t x) { return (x + 15) & ~int64_t(15); };
   const int64_t mm = up(pl.m * pl.m), NB = (int64_t)pl.P * pl.P;
   return sizeof(double) * (3 * up(NB * pl.RL) + 2 * up(pl.n * pl.n) + 2 * mm +
@@ -217,7 +254,7 @@ size_t tiny_smem(const Plan& pl) {
 
 cudaError_t launch_tiny(const Plan& pl, double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
-  const int cs = (int)std::min<int64_t>(8, pl.RL);
+  const int cs = tiny_cluster(pl);
   const size_t smem = tiny_smem(pl);
   static std::atomic<uint64_t> opted{0};  // >48 KB opt-in, once per device
   int dev = 0;
