@@ -1231,3 +1231,22 @@ def test_two_cta_leaf(name, levels, n, monkeypatch):
             assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all(), two
             out[two] = host(p.dgemm(dev(Ar), dev(Br)))
     assert (out["0"] == out["1"]).all()
+
+
+@pytest.mark.parametrize("n,bn", [(2048, "64"), (4096, "64"), (2048, "128")])
+def test_fused_ordered_concurrent_dependencies(n, bn, monkeypatch):
+    """The ordered fold where its flags really order concurrent CTAs: few tiles
+    per product (n = 2048: 16 / 32 tiles; n = 4096 with 64-wide tiles: 128), so
+    the products of one tile position run in the same wave and wait on each
+    other.  Five launches, each bitwise the flat unfused result."""
+    t = triples.get(SW)
+    A, B = mf_inputs.pair("uniform", n, 50)
+    monkeypatch.setenv("MF_LEAF_BN", bn)
+    Cf, Cu = _ordered_and_flat(monkeypatch, t, 2, n, A, B, 1.0)
+    assert (Cf == Cu).all()
+    with monkeypatch.context() as mp:
+        mp.setenv("MF_MIX_GENERIC", "1")
+        with mf.Plan(t, 2, n, fuse_postadd=1) as p:
+            Ad, Bd = dev(A), dev(B)
+            for _ in range(5):
+                assert (host(p.dgemm(Ad, Bd)) == Cu).all()
