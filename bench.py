@@ -644,12 +644,16 @@ def main():
         for label, levels, kw in (
                 (f"n={n} fp64, 3-level strassen-winograd (flattened <8,8,8;343>)", 3, {}),
                 (f"n={n} fp64, 3-level strassen-winograd, {ordered}", 3, {"fuse_postadd": 1}),
+                (f"n={n} fp64, 3-level strassen-winograd, post-additions fused by bulk f64 "
+                 "reductions into C (two CTAs per SM; order not fixed; no P workspace)", 3,
+                 {"fuse_postadd": 2}),
                 (f"n={n} fp64, 4-level strassen-winograd (one level by level, each of its 7 "
                  "products a flattened <8,8,8;343> child: 2401 leaves)", 4,
                  {"level_by_level": True, "recurse_levels": 1}),
                 (f"n={n} fp64, 2-level strassen-winograd, {ordered}", 2, {"fuse_postadd": 1}),
                 (f"n={n} fp64, 2-level strassen-winograd, post-additions fused by bulk f64 "
-                 "reductions into C (order not fixed; no P workspace)", 2, {"fuse_postadd": 2}),
+                 "reductions into C (two CTAs per SM; order not fixed; no P workspace)", 2,
+                 {"fuse_postadd": 2}),
                 (f"n={n} fp64, 2-level strassen-winograd with cuBLAS-batched leaves (ablation: "
                  "same K4/K6, cublasDgemmBatched leaf)", 2, {"leaf": "cublas"})):
             if n % (2 ** levels):
