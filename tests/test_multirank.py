@@ -274,3 +274,31 @@ def test_nccl_multiprocess_every_mode():
                 results.append([z[f"arr_{k}"] for k in range(len(z.files))])
             refs = [(k,) + inputs(k, n, 3 + i) for i, k in enumerate(("int1024", "uniform"))]
             check(assemble(results, N, out_mode), refs, levels, alpha)
+
+
+def test_loopback_random_sweep():
+    """24 random draws over triple (SW, Laderman, paper-Strassen, Strassen 1969),
+    levels, n (ragged leaves and uneven row splits included), N in 2..8,
+    input / output mode, comm regions, entry point and alpha, on loopback ranks:
+    exact on integers, within the bounds on random inputs, every rank equal
+    under MF_OUT_ALL."""
+    rng = np.random.Generator(np.random.PCG64(2026))
+    names = [SW, "laderman", "paper-strassen", "strassen-1969"]
+    for _ in range(24):
+        name = names[int(rng.integers(len(names)))]
+        p = 3 if name == "laderman" else 2
+        levels = 1 if name == "laderman" else int(rng.integers(1, 3))
+        N = int(rng.integers(2, 9))
+        R = (23 if p == 3 else 7) ** levels
+        if N > R:
+            N = R
+        out_mode = str(rng.choice(["root", "all", "rowslab"]))
+        unit = p ** levels
+        if out_mode == "rowslab":
+            unit = unit * N // np.gcd(unit, N)
+        n = unit * int(rng.integers(max(1, 256 // unit), max(2, 1100 // unit)))
+        in_mode = str(rng.choice(["root", "replicated"]))
+        regions = int(rng.choice([0, 1, 3]))
+        entry = str(rng.choice(["device", "host", "host_async"]))
+        alpha = float(rng.choice([1.0, -0.5, 2.0]))
+        run_loopback(N, name, levels, n, in_mode, out_mode, regions, entry, alpha=alpha)
