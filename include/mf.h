@@ -269,6 +269,24 @@ mf_status mf_plan_products(mf_plan_t plan, int32_t* a_src, int32_t* a_idx, int32
 mf_status mf_plan_kernels(mf_plan_t plan, int32_t* jit_tables, int32_t* jit_built,
                           int64_t* launches /* 4 */);
 
+/* The exchange schedule of one mf_dgemm call of a sharded plan (SURVEY §8e, row
+ * a6): the collectives this rank issues, in issue order, as mf_dgemm would with
+ * a communicator (host-only plans included, so CPU tests can replay them with
+ * another transport).  Op i: kind[i] = MF_X_BCAST / MF_X_REDUCE /
+ * MF_X_ALLREDUCE / MF_X_REDUCE_SCATTER; buf / recv_buf = MF_XB_A, MF_XB_B
+ * (the n x n inputs, ld n), MF_XB_C (the partial C, n x n, ld n) or MF_XB_COUT
+ * (this rank's n/N x n output slab, MF_OUT_ROWSLAB); off / recv_off / count in
+ * doubles (count per rank for a reduce-scatter); root rank; ops of one group
+ * are issued as one NCCL group; phase 0 = the MF_IN_ROOT input broadcasts (B's
+ * row slabs, then A's), phase 1 + k = the reduction of row region k (or of the
+ * whole partial C, phase 1).  *n_ops = number of ops (arrays: cap entries,
+ * any may be NULL); 0 for unsharded plans. */
+enum { MF_X_BCAST = 0, MF_X_REDUCE = 1, MF_X_ALLREDUCE = 2, MF_X_REDUCE_SCATTER = 3 };
+enum { MF_XB_A = 0, MF_XB_B = 1, MF_XB_C = 2, MF_XB_COUT = 3 };
+mf_status mf_plan_exchange(mf_plan_t plan, int32_t* kind, int32_t* buf, int64_t* off, int64_t* count,
+                           int32_t* root, int32_t* recv_buf, int64_t* recv_off, int32_t* group,
+                           int32_t* phase, int64_t cap, int64_t* n_ops);
+
 /* Product sharding: with shard_count = N, rank r computes
  * floor(R^L / N) whole products (a contiguous range) and, of each of the
  * R^L mod N leftover products (shard[q] = -1), the 128-aligned output row slab
@@ -369,7 +387,7 @@ mf_status mf_triple_kron(int32_t po, int32_t Ro, const double* Uo, const double*
  *    composing it with mf_triple_kron and planning levels = 1.
  *  - added entry points: mf_dgemm_host / _async / mf_host_sync (host
  *    buffers), mf_plan_products / mf_plan_shard_rows / mf_plan_kernels
- *    (introspection for tests), mf_premix / mf_leaf / mf_postmix (step-by-step
+ *    / mf_plan_exchange (introspection for tests), mf_premix / mf_leaf / mf_postmix (step-by-step
  *    parity), mf_profile_read (phase timing), mf_loop_comm_create /
  *    mf_comm_info / mf_comm_destroy (communicators), mf_jit_compile_check
  *    (generator check without a GPU), mf_version. */

@@ -42,7 +42,7 @@ EXPORTS = ("mf_plan", "mf_dgemm", "mf_dgemm_host", "mf_destroy", "mf_last_error"
            "mf_nccl_comm_create", "mf_nccl_comm_destroy", "mf_version", "mf_profile_read",
            "mf_plan_shard_rows", "mf_dgemm_host_async", "mf_host_sync", "mf_jit_compile_check",
            "mf_loop_comm_create", "mf_comm_info", "mf_comm_destroy", "mf_plan_kernels",
-           "mf_triple_kron")
+           "mf_triple_kron", "mf_plan_exchange")
 COMM_NCCL, COMM_LOOPBACK = 0, 1
 
 
@@ -73,6 +73,7 @@ _lib.mf_plan_info.argtypes = [_P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTE
 _lib.mf_plan_products.argtypes = [_P] * 7
 _lib.mf_plan_shard_rows.argtypes = [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
 _lib.mf_plan_kernels.argtypes = [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32), _P]
+_lib.mf_plan_exchange.argtypes = [_P] * 10 + [_I64, ctypes.POINTER(_I64)]
 _lib.mf_premix.argtypes = [_P, _I32, _P, _I64, _P, _P]
 _lib.mf_leaf.argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _P, _P]
 _lib.mf_postmix.argtypes = [_P, _D, _P, _P, _I64, _P]
@@ -229,6 +230,18 @@ class Plan:
         _check(_lib.mf_plan_kernels(self._h, ctypes.byref(jt), ctypes.byref(jb), launches))
         return {"jit_tables": jt.value, "jit_built": jb.value,
                 "launches": dict(zip(self.KERNEL_KINDS, list(launches)))}
+
+    def exchange(self) -> list:
+        """mf_plan_exchange: the collectives one mf_dgemm call of this rank issues, in
+        order -- dicts with kind, buf, off, count, root, recv_buf, recv_off, group, phase."""
+        n = _I64()
+        _check(_lib.mf_plan_exchange(self._h, *([None] * 9), 0, ctypes.byref(n)))
+        cols = {k: np.zeros(n.value, dtype=np.int64 if k in ("off", "count", "recv_off") else np.int32)
+                for k in ("kind", "buf", "off", "count", "root", "recv_buf", "recv_off", "group", "phase")}
+        _check(_lib.mf_plan_exchange(self._h, *[cols[k].ctypes.data for k in
+                                                ("kind", "buf", "off", "count", "root", "recv_buf",
+                                                 "recv_off", "group", "phase")], n.value, ctypes.byref(n)))
+        return [{k: int(v[i]) for k, v in cols.items()} for i in range(n.value)]
 
     def shard_rows(self) -> tuple:
         """Row slab [r0, r1) this rank computes of each split product (0, 0 if none)."""

@@ -1064,12 +1064,12 @@ static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n);
 // Row regions of the region-overlapped exchange (mf_options.comm_regions).
 // Without a communicator only an explicit comm_regions > 1 applies (the regions
 // are computed, nothing is reduced: the emulated ranks' partial C, for tests).
-static int comm_regions(const Plan& pl) {
+static int comm_regions(const Plan& pl, bool with_comm) {
   if (pl.child || pl.fuse || !pl.batches.empty() || pl.levels == 0 ||
-      (!pl.comm && pl.opt.comm_regions <= 1))
+      (!with_comm && pl.opt.comm_regions <= 1))
     return 1;
   const int want = pl.opt.comm_regions > 0 ? pl.opt.comm_regions
-                                           : (pl.comm && pl.shard_count > 1 ? 8 : 1);
+                                           : (with_comm && pl.shard_count > 1 ? 8 : 1);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (pl.m + 127) / 128));
 }
 
@@ -1114,6 +1114,123 @@ mf_status mf_dgemm(mf_plan_t pl, double alpha, const double* A, int64_t lda, con
   }
   pl->g_key = key;
   MF_CUDA(cudaGraphLaunch(pl->g_exec, s), "cudaGraphLaunch");
+  return MF_OK;
+}
+
+// ---- exchange schedule (a6): the collectives a rank issues, in order ----
+// One generator serves mf_dgemm (which executes the ops) and mf_plan_exchange
+// (which returns them, so CPU tests can replay the schedule with gloo).
+// Offsets / counts in doubles, relative to the buffer named by buf / recv_buf
+// (XB_A, XB_B: the n x n inputs, ld n; XB_C: the partial C, ld n; XB_COUT: this
+// rank's output slab under MF_OUT_ROWSLAB).  Ops with one `group` id are issued
+// in one group; `event` >= 0: the input slab event recorded after the group.
+static std::pair<int64_t, int64_t> tile_piece(int64_t m, int i, int n);
+
+static void input_schedule(const Plan& pl, int KI, std::vector<XOp>& ops) {
+  const int64_t m = pl.m, n = pl.n;
+  int group = 0;
+  // B first: every product needs all of S_q, while the leaf's row region k
+  // needs only A's slab k -- so region k can start when A's slab k landed
+  for (int side = 1; side >= 0; --side)
+    for (int k = 0; k < KI; ++k, ++group) {
+      const auto sr = tile_piece(m, k, KI);
+      for (int br = 0; br < pl.P && sr.second > sr.first; ++br) {
+        XOp o{};
+        o.kind = XK_BCAST;
+        o.buf = o.recv_buf = side == 0 ? XB_A : XB_B;
+        o.off = o.recv_off = (br * m + sr.first) * n;
+        o.count = (sr.second - sr.first) * n;
+        o.root = 0;
+        o.group = group;
+        o.event = -1;
+        ops.push_back(o);
+      }
+      if (!ops.empty() && ops.back().group == group) ops.back().event = side * KI + k;
+    }
+}
+
+// region rows [r0, r1) of every block row of the partial C (MF_OUT_ROWSLAB:
+// cut at the owners' output slabs and reduced onto each owner)
+static void region_schedule(const Plan& pl, int64_t r0, int64_t r1, int group, std::vector<XOp>& ops) {
+  const int64_t m = pl.m, n = pl.n, slab = n / pl.shard_count;
+  for (int br = 0; br < pl.P; ++br) {
+    const int64_t row0 = br * m + r0, row1 = br * m + r1;
+    if (pl.opt.output_mode == MF_OUT_ROWSLAB) {
+      for (int64_t o = row0 / slab; o * slab < row1; ++o) {
+        const int64_t a = std::max<int64_t>(row0, o * slab), b = std::min<int64_t>(row1, (o + 1) * slab);
+        XOp x{};
+        x.kind = XK_REDUCE;
+        x.buf = XB_C;
+        x.off = a * n;
+        x.count = (b - a) * n;
+        x.root = (int32_t)o;
+        x.recv_buf = o == pl.shard_rank ? XB_COUT : XB_C;
+        x.recv_off = o == pl.shard_rank ? (a - o * slab) * n : a * n;
+        x.group = group;
+        x.event = -1;
+        ops.push_back(x);
+      }
+    } else {
+      XOp x{};
+      x.kind = pl.opt.output_mode == MF_OUT_ALL ? XK_ALLREDUCE : XK_REDUCE;
+      x.buf = x.recv_buf = XB_C;
+      x.off = x.recv_off = row0 * n;
+      x.count = (row1 - row0) * n;
+      x.root = 0;
+      x.group = group;
+      x.event = -1;
+      ops.push_back(x);
+    }
+  }
+}
+
+// one collective on the whole partial C (no region schedule)
+static void final_schedule(const Plan& pl, int group, std::vector<XOp>& ops) {
+  const int64_t n = pl.n;
+  XOp x{};
+  x.buf = XB_C;
+  x.root = 0;
+  x.group = group;
+  x.event = -1;
+  if (pl.opt.output_mode == MF_OUT_ROWSLAB) {
+    x.kind = XK_REDUCE_SCATTER;
+    x.count = (n / pl.shard_count) * n;  // per rank
+    x.recv_buf = XB_COUT;
+  } else {
+    x.kind = pl.opt.output_mode == MF_OUT_ALL ? XK_ALLREDUCE : XK_REDUCE;
+    x.count = n * n;
+    x.recv_buf = XB_C;
+  }
+  ops.push_back(x);
+}
+
+// issue ops[i0, i1) (whole groups) on stream s; base[b] = the buffer of XB_* b
+static mf_status exec_ops(Comm* xc, const std::vector<XOp>& ops, size_t i0, size_t i1, double* const base[4],
+                          cudaStream_t s, const std::vector<cudaEvent_t>* events) {
+  mf_status st = MF_OK;
+  for (size_t i = i0; i < i1;) {
+    const int g = ops[i].group;
+    if ((st = xc->group_start()) != MF_OK) return st;
+    int ev = -1;
+    for (; i < i1 && ops[i].group == g; ++i) {
+      const XOp& o = ops[i];
+      double* src = base[o.buf] + o.off;
+      double* dst = base[o.recv_buf] + o.recv_off;
+      switch (o.kind) {
+        case XK_BCAST: st = xc->bcast(src, (size_t)o.count, o.root, s); break;
+        case XK_REDUCE: st = xc->reduce(src, dst, (size_t)o.count, o.root, s); break;
+        case XK_ALLREDUCE: st = xc->allreduce(src, dst, (size_t)o.count, s); break;
+        default: st = xc->reduce_scatter(src, dst, (size_t)o.count, s); break;
+      }
+      if (st != MF_OK) {
+        xc->group_end();
+        return st;
+      }
+      if (o.event >= 0) ev = o.event;
+    }
+    if ((st = xc->group_end()) != MF_OK) return st;
+    if (ev >= 0 && events) MF_CUDA(cudaEventRecord((*events)[ev], s), "event");
+  }
   return MF_OK;
 }
 
@@ -1204,23 +1321,10 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
     // the previous call's reads of the replicas)
     MF_CUDA(cudaEventRecord(pl->in_events[2 * KI + 1], s), "event");
     MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->in_events[2 * KI + 1], 0), "wait");
-    // B first: every product needs all of S_q, while the leaf's row region k
-    // needs only A's slab k -- so region k can start when A's slab k landed
-    for (int side = 1; side >= 0; --side) {
-      double* buf = side == 0 ? bufA : bufB;
-      for (int k = 0; k < KI; ++k) {
-        const auto sr = tile_piece(m, k, KI);
-        if ((st = xc->group_start()) != MF_OK) return st;
-        for (int br = 0; br < pl->P && sr.second > sr.first; ++br)
-          if ((st = xc->bcast(buf + (br * m + sr.first) * n, (size_t)(sr.second - sr.first) * n, 0,
-                              pl->comm_s)) != MF_OK) {
-            xc->group_end();
-            return st;
-          }
-        if ((st = xc->group_end()) != MF_OK) return st;
-        MF_CUDA(cudaEventRecord(pl->in_events[side * KI + k], pl->comm_s), "event");
-      }
-    }
+    std::vector<XOp> ops;
+    input_schedule(*pl, KI, ops);
+    double* const base[4] = {bufA, bufB, nullptr, nullptr};
+    if ((st = exec_ops(xc, ops, 0, ops.size(), base, pl->comm_s, &pl->in_events)) != MF_OK) return st;
     MF_CUDA(cudaEventRecord(pl->in_events[2 * KI], pl->comm_s), "event");  // all landed
     A = bufA; lda = n; B = bufB; ldb = n;
   }
@@ -1255,7 +1359,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
   };
   // MF_IN_ROOT with the region schedule: K4(A) of slab k runs right before the
   // leaf's region k (same rows), so A's broadcast overlaps the leaf, not only K4
-  const bool a_by_region = wait_inputs && levels_flat(*pl) && comm_regions(*pl) == KI && KI > 1;
+  const bool a_by_region = wait_inputs && levels_flat(*pl) && comm_regions(*pl, pl->comm != nullptr) == KI && KI > 1;
   // K4 of one side for this shard (whole products' slots, then the split
   // products' slots on the rank's row slab), slab by slab behind the input
   // broadcast when this rank receives its inputs
@@ -1359,7 +1463,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
                            pl->Pw + (int64_t)pl->loc_q[q] * mm, m, stream)) != MF_OK)
           return st;
       }
-    } else if (comm_regions(*pl) > 1) {
+    } else if (comm_regions(*pl, pl->comm != nullptr) > 1) {
       // a3 + a4 + a6 by row regions (NEXT-4): region k's leaf products and
       // post-addition, then its rows of the partial C (one contiguous piece per
       // block row) are summed on the exchange stream while region k+1
@@ -1367,7 +1471,7 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
       // (MF_OUT_ALL), or onto the rank whose output row slab holds them
       // (MF_OUT_ROWSLAB: a region-wise reduce-scatter).  Every rank issues the
       // same collectives in the same order.
-      const int K = comm_regions(*pl);
+      const int K = comm_regions(*pl, pl->comm != nullptr);
       if (!pl->comm_s) MF_CUDA(cudaStreamCreateWithFlags(&pl->comm_s, cudaStreamNonBlocking), "stream");
       if ((st = ensure_events(pl->comm_events, (size_t)K + 1)) != MF_OK) return st;
       const bool exchange = xc != nullptr;
@@ -1380,7 +1484,6 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
       };
       MF_CUDA(cudaEventRecord(pl->comm_events[K], s), "event");
       MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->comm_events[K], 0), "wait");  // exchange after K4
-      const int64_t slab = n / pl->shard_count;  // MF_OUT_ROWSLAB rows per rank
       for (int k = 0; k < K; ++k) {
         const auto rg = tile_piece(m, k, K);
         if (rg.second <= rg.first) continue;
@@ -1410,29 +1513,10 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
         if (!exchange) continue;
         MF_CUDA(cudaEventRecord(pl->comm_events[k], s), "event");
         MF_CUDA(cudaStreamWaitEvent(pl->comm_s, pl->comm_events[k], 0), "wait");
-        if ((st = xc->group_start()) != MF_OK) return st;
-        for (int br = 0; br < pl->P; ++br) {
-          const int64_t row0 = br * m + rg.first, row1 = br * m + rg.second;
-          double* piece = C + row0 * n;
-          if (rowslab) {
-            // the rows of this piece owned by each rank's output slab
-            for (int64_t o = row0 / slab; o * slab < row1; ++o) {
-              const int64_t a = std::max<int64_t>(row0, o * slab), b = std::min<int64_t>(row1, (o + 1) * slab);
-              double* recv = o == pl->shard_rank ? C_out + (a - o * slab) * n : C + a * n;
-              st = xc->reduce(C + a * n, recv, (size_t)(b - a) * n, (int)o, pl->comm_s);
-              if (st != MF_OK) break;
-            }
-          } else {
-            const size_t count = (size_t)(row1 - row0) * n;
-            st = pl->opt.output_mode == MF_OUT_ALL ? xc->allreduce(piece, piece, count, pl->comm_s)
-                                                   : xc->reduce(piece, piece, count, 0, pl->comm_s);
-          }
-          if (st != MF_OK) {
-            xc->group_end();
-            return st;
-          }
-        }
-        if ((st = xc->group_end()) != MF_OK) return st;
+        std::vector<XOp> ops;
+        region_schedule(*pl, rg.first, rg.second, k, ops);
+        double* const base[4] = {nullptr, nullptr, C, C_out};
+        if ((st = exec_ops(xc, ops, 0, ops.size(), base, pl->comm_s, nullptr)) != MF_OK) return st;
       }
       MF_CUDA(cudaEventRecord(pl->comm_events[K], pl->comm_s), "event");
       MF_CUDA(cudaStreamWaitEvent(s, pl->comm_events[K], 0), "wait");
@@ -1467,15 +1551,56 @@ static mf_status dgemm_eager(mf_plan_t pl, double alpha, const double* A, int64_
   mark(4);
   if (xc && !reduced) {
     // a6: sum the partial C over ranks (NCCL over NVLink/NVSwitch)
-    st = rowslab ? xc->reduce_scatter(C, C_out, (size_t)c_rows * n, s)
-         : pl->opt.output_mode == MF_OUT_ALL ? xc->allreduce(C, C, (size_t)n * n, s)
-                                             : xc->reduce(C, C, (size_t)n * n, 0, s);
-    if (st != MF_OK) return st;
+    std::vector<XOp> ops;
+    final_schedule(*pl, 0, ops);
+    double* const base[4] = {nullptr, nullptr, C, C_out};
+    if ((st = exec_ops(xc, ops, 0, ops.size(), base, s, nullptr)) != MF_OK) return st;
   }
   // the call's stream ends after the input broadcast (rank 0 sends from the
   // caller's A and B, which must stay untouched until then)
   if (root_inputs) MF_CUDA(cudaStreamWaitEvent(s, pl->in_events[2 * KI], 0), "wait");
   mark(5);
+  return MF_OK;
+}
+
+mf_status mf_plan_exchange(mf_plan_t pl, int32_t* kind, int32_t* buf, int64_t* off, int64_t* count,
+                           int32_t* root, int32_t* recv_buf, int64_t* recv_off, int32_t* group,
+                           int32_t* phase, int64_t cap, int64_t* n_ops) {
+  g_err.clear();
+  if (!pl || !n_ops) return fail(MF_ERR_INVALID_ARG, "plan or n_ops is NULL");
+  if (pl->shard_count < 2) { *n_ops = 0; return MF_OK; }
+  std::vector<XOp> ops;
+  std::vector<int32_t> ph;
+  if (pl->opt.input_mode == MF_IN_ROOT && pl->levels > 0) {
+    input_schedule(*pl, input_slabs(*pl), ops);
+    ph.assign(ops.size(), 0);
+  }
+  const int K = comm_regions(*pl, true);
+  int g0 = ops.empty() ? 0 : ops.back().group + 1;
+  if (K > 1) {
+    for (int k = 0; k < K; ++k) {
+      const auto rg = tile_piece(pl->m, k, K);
+      if (rg.second <= rg.first) continue;
+      region_schedule(*pl, rg.first, rg.second, g0 + k, ops);
+      ph.resize(ops.size(), 1 + k);
+    }
+  } else {
+    final_schedule(*pl, g0, ops);
+    ph.resize(ops.size(), 1);
+  }
+  *n_ops = (int64_t)ops.size();
+  for (size_t i = 0; i < ops.size() && (int64_t)i < cap; ++i) {
+    const XOp& o = ops[i];
+    if (kind) kind[i] = o.kind;
+    if (buf) buf[i] = o.buf;
+    if (off) off[i] = o.off;
+    if (count) count[i] = o.count;
+    if (root) root[i] = o.root;
+    if (recv_buf) recv_buf[i] = o.recv_buf;
+    if (recv_off) recv_off[i] = o.recv_off;
+    if (group) group[i] = o.group;
+    if (phase) phase[i] = ph[i];
+  }
   return MF_OK;
 }
 

@@ -43,6 +43,17 @@ struct Comm {
 };
 Comm* comm_from(void* handle);  // nullptr if handle is not a Comm of this library
 
+// One collective of the exchange schedule (mf_api.cpp; mf_plan_exchange).
+enum XKind : int32_t { XK_BCAST = 0, XK_REDUCE = 1, XK_ALLREDUCE = 2, XK_REDUCE_SCATTER = 3 };
+enum XBuf : int32_t { XB_A = 0, XB_B = 1, XB_C = 2, XB_COUT = 3 };
+struct XOp {
+  int32_t kind, buf;        // XKind; the send buffer (XBuf)
+  int64_t off, count;       // doubles (count: per rank for a reduce-scatter)
+  int32_t root, recv_buf;   // root rank; the receive buffer
+  int64_t recv_off;
+  int32_t group, event;     // issued together; input slab event after the group (-1: none)
+};
+
 // Largest flattened split factor P = p^levels the mix kernels are built for
 // (P^2 <= 81 blocks: p=9 one level, p=3 two levels, p=2 up to three levels).
 constexpr int kMaxBlocks = 81;
