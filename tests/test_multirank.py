@@ -302,3 +302,50 @@ def test_loopback_random_sweep():
         entry = str(rng.choice(["device", "host", "host_async"]))
         alpha = float(rng.choice([1.0, -0.5, 2.0]))
         run_loopback(N, name, levels, n, in_mode, out_mode, regions, entry, alpha=alpha)
+
+
+@pytest.mark.parametrize("out_mode", ["root", "rowslab"])
+def test_loopback_bench_size_eight_ranks(out_mode):
+    """The bench's sharded workload at full size: SW^2, n = 16384, 8 ranks
+    (6 whole products + a 512-row slab of product 48 each), MF_IN_ROOT slab
+    broadcasts under K4 and the leaf regions, 8 region reductions -- exact
+    Freivalds on integers and sampled oracle entries on random inputs."""
+    n, N = 16384, 8
+    res = {}
+    for kind in ("int1024", "uniform"):
+        Ad, Bd = mf_inputs.device_pair(kind, n, 60 if kind == "int1024" else 61)
+        comms = mf.loop_comm_create(N)
+        out, errs = [None] * N, []
+
+        def worker(r):
+            try:
+                torch.cuda.set_device(0)
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st), mf.Plan(triples.get(SW), 2, n, comm=comms[r], shard_rank=r,
+                                                    shard_count=N, input_mode=IN["root"],
+                                                    output_mode=OUT[out_mode]) as p:
+                    C = p.dgemm(Ad if r == 0 else None, Bd if r == 0 else None, stream=st)
+                    st.synchronize()
+                    if out_mode == "rowslab" or r == 0:
+                        out[r] = C.cpu().numpy()
+            except BaseException as e:  # noqa: BLE001
+                errs.append((r, repr(e)))
+
+        th = [threading.Thread(target=worker, args=(r,)) for r in range(N)]
+        [t.start() for t in th]
+        [t.join(timeout=900) for t in th]
+        for c in comms:
+            mf.comm_destroy(c)
+        assert not errs, errs
+        C = np.concatenate(out) if out_mode == "rowslab" else out[0]
+        res[kind] = (Ad.cpu().numpy(), Bd.cpu().numpy(), C)
+        del Ad, Bd
+        torch.cuda.empty_cache()
+    A, B, C = res["int1024"]
+    assert oracle.freivalds_int(A, B, C, trials=2) == 0
+    A, B, C = res["uniform"]
+    rng = np.random.Generator(np.random.PCG64(7))
+    rows, cols = rng.integers(0, n, 256), rng.integers(0, n, 256)
+    ref = oracle.sample_entries(A, B, rows, cols)
+    err = float(np.abs(C[rows, cols] - ref).max()) / (n * np.abs(A).max() * np.abs(B).max())
+    assert_error(err, 2)
