@@ -136,7 +136,7 @@ typedef struct {
                            host call instead of four launches: the n <= 4096
                            configs are host-issue bound).  Ignored on the
                            legacy default stream (NULL) and with profile,
-                           nccl_comm, level_by_level or MF_LEAF_CUBLAS      */
+                           comm, level_by_level or MF_LEAF_CUBLAS           */
   int32_t comm_regions;   /* sharded plans with comm: the leaf and post-addition
                            run in this many 128-aligned row regions, and each
                            region's rows of C are summed on the exchange stream
