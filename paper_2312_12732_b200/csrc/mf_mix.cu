@@ -331,14 +331,10 @@ static cudaError_t mix_dispatch(int vw, const MixTable& t, View in, View out, in
 cudaError_t launch_premix(const Plan& pl, const MixTable& t, const double* X, int64_t ldx,
                           double* out, cudaStream_t s, Rows rows) {
   if (t.nrow == 0 || rows.end(pl.m) <= rows.r0 || rows.cend(pl.m) <= rows.c0) return cudaSuccess;
-  // specialised kernels serve the plan's own tables; the shard's product mask
-  // selects the outputs (A: whole products, or split products on their rows)
+  // specialised kernels serve the plan's own tables (unsharded plans: a shard's
+  // tables use local slot numbering and run generated kernels)
   const bool own = &t == &pl.mixA || &t == &pl.mixA2 || &t == &pl.mixB;
   if (pl.fixed_id > 0 && own) {
-    if (pl.shard_count > 1 && t.jit_fn) {  // a shard's own slots (see mf_plan)
-      const cudaError_t j = jit_launch(t, X, ldx, out, pl.m, pl.m, 1.0, rows, 0, s);
-      if (j != cudaErrorNotSupported) return ++pl.mix_launches[MIXK_JIT], j;
-    }
     const int side = &t == &pl.mixB ? 1 : 0;
     const ProdMask& mask = &t == &pl.mixA ? pl.mask_whole : (&t == &pl.mixA2 ? pl.mask_part : pl.mask_all);
     if (pl.fixed_id >= 8)
