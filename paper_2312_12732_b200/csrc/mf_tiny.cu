@@ -50,9 +50,15 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 
 // one term of an ascending combination, the oracle's rule (DESIGN R7):
 // acc starts at -0.0; +-1 terms add / subtract, others multiply then add
-__device__ __forceinline__ double term(double acc, double c, double x) {
-  return __dadd_rn(acc, c == 1.0 ? x : (c == -1.0 ? -x : __dmul_rn(c, x)));
+// the same rule with the coefficient's kind decided outside the element loop
+// (0 absent, 1: +x, 2: -x, 3: c*x): no floating-point compares per element
+__device__ __forceinline__ int coef_kind(double c) {
+  return c == 0.0 ? 0 : (c == 1.0 ? 1 : (c == -1.0 ? 2 : 3));
 }
+__device__ __forceinline__ double kterm(double acc, int kind, double c, double x) {
+  return kind == 1 ? __dadd_rn(acc, x) : (kind == 2 ? __dadd_rn(acc, -x) : __dadd_rn(acc, __dmul_rn(c, x)));
+}
+
 
 __global__ void __launch_bounds__(TINY_THREADS)
 tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
@@ -112,17 +118,28 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
   __syncthreads();
   TSTAMP(1);
   for (int q = me, j = 0; q < R; q += cs, ++j) {
-    // T_q, S_q: block k of X is rows (k/P)*m.., cols (k%P)*m..
+    // T_q, S_q: block k of X is rows (k/P)*m.., cols (k%P)*m..;
+    // the product's coefficients, their kinds and the block offsets sit in
+    // registers while the threads sweep its elements (NB <= 16 here)
+    double cu[16], cv[16];
+    int ku[16], kv[16], boff[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      cu[k] = k < NB ? sU[k * R + q] : 0.0;
+      cv[k] = k < NB ? sV[k * R + q] : 0.0;
+      ku[k] = coef_kind(cu[k]);
+      kv[k] = coef_kind(cv[k]);
+      boff[k] = k < NB ? (k / P) * m * n + (k % P) * m : 0;
+    }
     for (int e = threadIdx.x; e < mm; e += blockDim.x) {
-      const int r = e / m, c = e - r * m;
+      const int r = e / m, c = e - r * m, rcn = r * n + c;
       double t = -0.0, s = -0.0;
-      int off = r * n + c;  // block (kr, kc): + kr*m*n + kc*m, stepped without division
-      for (int kr = 0, k = 0; kr < P; ++kr, off += m * n - P * m)
-        for (int kc = 0; kc < P; ++kc, ++k, off += m) {
-          const double u = sU[k * R + q], v = sV[k * R + q];
-          if (u != 0.0) t = term(t, u, sA[off]);
-          if (v != 0.0) s = term(s, v, sB[off]);
-        }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k >= NB) break;
+        if (ku[k]) t = kterm(t, ku[k], cu[k], sA[boff[k] + rcn]);
+        if (kv[k]) s = kterm(s, kv[k], cv[k], sB[boff[k] + rcn]);
+      }
       sT[e] = t;
       sS[e] = s;
     }
@@ -211,9 +228,11 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
   for (int e = tid; e < NB * mm; e += nth) {
     const int i = e / mm, rc = e - i * mm;
     double acc = -0.0;
+    const double* wi = sW + i * R;
     for (int q = 0; q < R; ++q) {
-      const double w = sW[i * R + q];
-      if (w != 0.0) acc = term(acc, w, sAll[(size_t)q * mmp + rc]);
+      const double w = wi[q];
+      const int kw = coef_kind(w);
+      if (kw) acc = kterm(acc, kw, w, sAll[(size_t)q * mmp + rc]);
     }
     if (alpha != 1.0) acc = __dmul_rn(alpha, acc);
     const int r = rc / m, c = rc - r * m;
@@ -235,7 +254,7 @@ size_t tiny_smem(const Plan& pl);
 bool tiny_eligible(const Plan& pl) {
   return pl.levels > 0 && pl.n <= 64 && pl.RL <= 64 && !pl.child && pl.batches.empty() &&
          !pl.fuse && pl.shard_count == 1 && !pl.comm && pl.leaf == MF_LEAF_DMMA &&
-         pl.d_tinyU != nullptr && tiny_smem(pl) <= 200 * 1024;
+         pl.d_tinyU != nullptr && (int64_t)pl.P * pl.P <= 16 && tiny_smem(pl) <= 200 * 1024;
 }
 
 static int tiny_cluster(const Plan& pl) {
