@@ -577,8 +577,21 @@ def main():
     # ---- end to end through the C ABI with host buffers (every rank: its
     # replicated host inputs in, the NCCL reduce inside, C back; max over ranks) ----
     if not a.no_e2e:
+        # N > 1 with host buffers: every rank holds the host inputs and copies only
+        # its 1/N row slab over its own PCIe link; NCCL all-gathers the rest (one
+        # host link carrying all of A and B would bound the step at N = 8)
+        slab_e2e = distributed and world > 1 and n % world == 0
+        eplan = plan
+        if slab_e2e:
+            eplan = mf.Plan(triple, a.levels, n, device=local, shard_rank=rank, shard_count=world,
+                            comm=comm, level_by_level=a.level_by_level,
+                            max_workspace=int(a.max_workspace_gb * 1e9), fuse_postadd=a.fuse,
+                            recurse_levels=a.recurse_levels, leaf=a.leaf, comm_regions=a.comm_regions,
+                            input_mode=mf.IN_REPLICATED)
+            if not feeds:
+                A, B = mf_inputs.device_pair("uniform", n, 0, device=f"cuda:{local}")
         Ch = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        if feeds:
+        if feeds or slab_e2e:
             Ah = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
             Bh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
             Ah.copy_(A); Bh.copy_(B)
@@ -604,18 +617,20 @@ def main():
             return dt
         # a stream of K products through mf_dgemm_host_async (call k+1's copies
         # under call k's compute), and single synchronous calls
-        dt = e2e_time(plan.dgemm_host_async_ptr, plan.host_sync)
-        dts = e2e_time(plan.dgemm_host_ptr, lambda: None)
+        dt = e2e_time(eplan.dgemm_host_async_ptr, eplan.host_sync)
+        dts = e2e_time(eplan.dgemm_host_ptr, lambda: None)
+        if eplan is not plan:
+            eplan.close()
         out["e2e"] = {"value": 2.0 * n ** 3 / dt / 1e12, "unit": UNIT, "ms_per_step": dt * 1e3,
                       "h2d_bytes_per_step": 2 * 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
                       "api": "mf_dgemm_host_async x K steps + mf_host_sync (pinned host A, B, C; "
                              "every step's H2D + compute + D2H inside the timed region; consecutive "
                              "steps overlap copies with compute"
-                             + (("; product-sharded: rank 0 copies A and B in and broadcasts them "
-                                 "by row slabs over NVLink under the other ranks' K4"
-                                 if in_root else
-                                 "; product-sharded: each rank copies its 1/N row slab of A and B "
-                                 "over its own PCIe link and NCCL all-gathers the rest over NVLink")
+                             + (("; product-sharded: each rank copies its 1/N row slab of A and B "
+                                 "over its own PCIe link and NCCL all-gathers the rest over NVLink"
+                                 if slab_e2e or not in_root else
+                                 "; product-sharded: rank 0 copies A and B in and broadcasts them "
+                                 "by row slabs over NVLink under the other ranks' K4 and leaf")
                                 + ", the NCCL reduce of C runs inside, C returns to rank 0's host "
                                   "buffer)" if distributed else ")"),
                       "sync": {"value": 2.0 * n ** 3 / dts / 1e12, "ms_per_step": dts * 1e3,
