@@ -58,6 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
               "-I", nccl_include()]
+    cmds = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src + ".o")
@@ -74,7 +75,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd += ["-x", "cu"]  # host-only TU compiled by nvcc for the CUDA headers
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
+    # translation units compile in parallel (the specialised-kernel units dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl", "-lpthread"]
         if verbose:
