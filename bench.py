@@ -155,6 +155,21 @@ def model_guard(levels):
     return 10 * 1e-16 * 2.0 ** max(1, levels)
 
 
+def step_roofline(a, n, ms, world, peak):
+    R = _rank(a)
+    p = 1
+    for part in a.triple.split("(x)"):
+        p *= {"laderman": 3, "classical-p3": 3}.get(part, 2)
+    alg = (R / p ** 3) ** a.levels * 2.0 * n ** 3  # R^L (n/p^L)^3 multiply-adds x 2
+    eff = 2.0 * n ** 3 / (ms * 1e-3) / 1e12
+    alg_tf = alg / (ms * 1e-3) / 1e12
+    return {"effective_tflops": eff, "algorithmic_tflops": alg_tf, "n_gpus": world,
+            "peak_tflops": peak * world, "effective_frac_of_peak": eff / (peak * world),
+            "algorithmic_frac_of_peak": alg_tf / (peak * world),
+            "note": "algorithmic = the leaf multiplications the method performs, R^L * 2 (n/p^L)^3, "
+                    "per second of the whole step (additions and exchange included)"}
+
+
 def launches_per_step(a):
     """Our kernels per mf_dgemm: K4, K4, K5, K6 per flattened level (K6 folded
     into K5 with --fuse); level by level: the top level's K4, K4, K6 around R
@@ -488,7 +503,11 @@ def main():
            "value_median": 2.0 * n ** 3 / (ms_median * 1e-3) / 1e12,
            "config": config(a, world), "clocks": clk,
            "gpu_launches": launches_per_step(a) * a.steps,
-           "roofline": roofline}
+           "roofline": roofline,
+           # the whole step against the FP64 tensor roofline of all N GPUs:
+           # effective rate, and the algorithmic rate (the multiplications the method
+           # performs, R^L 2 m^3 per product) -- the "without credit" fraction
+           "step_roofline": step_roofline(a, n, ms, world, peak)}
 
     # ---- accuracy (north_star: the scaled error against the definition
     # C_ij = sum_k A_ik B_kj, in extended precision on sampled entries; and
