@@ -820,13 +820,16 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     // epilogue runs beside the other's k loop.  The default for the
     // bulk-reduction fold, whose epilogue (stage + bulk reductions) it hides:
     // SW^2 n=16384 step 191.3 -> 187.9 ms, equal to the unfused step
-    // (profiles/leaf2cta_r02.jsonl); the unfused leaf keeps one 128 x 128 CTA
-    // per SM (184.2 vs 185.1 ms).  MF_LEAF_2CTA=1/0 forces it on/off.  Not for
+    // (profiles/leaf2cta_r02.jsonl).  Also the unfused default for m <= 1536,
+    // where the per-tile prologue / epilogue is a larger share of a tile's k
+    // loop: +0.4% (m = 1536) .. +9% (m = 512), SW^4 hybrid 158.2 -> 156.7 ms;
+    // above that one 128 x 128 CTA per SM (m = 4096: 184.2 vs 185.1 ms;
+    // profiles/leaf2cta_m_r02.jsonl).  MF_LEAF_2CTA=1/0 forces it on/off.  Not for
     // the ordered fold: with two CTAs per SM its flag-ordered read-modify-
     // writes lost updates in rows of warps 2-3 (a race not understood;
     // tools/ordered_pattern.py), so that fold keeps one CTA per SM.
     const char* e2 = getenv("MF_LEAF_2CTA");
-    const bool two_cta = !ordered && (e2 ? atoi(e2) > 0 : (a.post != nullptr));
+    const bool two_cta = !ordered && (e2 ? atoi(e2) > 0 : (a.post != nullptr || a.m <= 1536));
     if (two_cta) { cfg.bn = 64; cfg.split = 1; }
     const int bn = cfg.bn;
     // k sub-blocks of 16 per pipeline stage: 2 (k = 32, 3-stage ring), or 3

@@ -1217,7 +1217,8 @@ def test_random_shape_sweep():
 @pytest.mark.parametrize("name,levels,n", [(SW, 2, 2048), (SW, 1, 400), ("laderman", 1, 390), (None, 0, 640)])
 def test_two_cta_leaf(name, levels, n, monkeypatch):
     """The two-CTA-per-SM leaf (4 MMA warps, 128 x 64 tiles; the default under
-    the bulk-reduction fold, forced here for the unfused path): integer inputs
+    the bulk-reduction fold and for unfused leaves with m <= 1536; forced on and
+    off here): integer inputs
     exact, random inputs bitwise the one-CTA leaf (same k order per element)
     with no split-K tail on either side; ragged leaves (m = 200, 130) too."""
     t = triples.get(name) if name else None
