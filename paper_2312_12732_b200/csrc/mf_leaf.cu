@@ -394,6 +394,15 @@ leaf_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (gg + 2 < 2 * KSUB) {
         load_frags(sA, sB, gg + 2, fa0, fb0);
       } else {                               // last group: release, prefetch next stage
+        // The slot is refilled by TMA (async proxy) once every warp has
+        // arrived: its fragment loads (generic proxy) must have read the slot
+        // first.  mbarrier.arrive's release does not order them against the
+        // async proxy, and the SASS issued the arrive with the last LDS.128s
+        // still in flight -- measured: a fragment of the next stage's data in
+        // rows 64-127 of some tiles (ordered fold, two CTAs per SM, n >= 8192;
+        // tools/ordered_dbg.py).  The proxy fence waits for them (MEMBAR.ALL.CTA
+        // + FENCE.VIEW.ASYNC.S), after 64 DMMAs that cover their latency.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * s);
         if (kb + 1 < nk) {
@@ -817,19 +826,16 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (cfg.split > 1 && (!a.split_ws || a.split_ws_elems < cfg.ws_elems || a.split_cnt_len < cfg.n_tail))
       cfg.split = 1;
     // Two CTAs per SM (4 MMA warps, 128 x 64 tiles, 96 KB rings): one CTA's
-    // epilogue runs beside the other's k loop.  The default for the
-    // bulk-reduction fold, whose epilogue (stage + bulk reductions) it hides:
-    // SW^2 n=16384 step 191.3 -> 187.9 ms, equal to the unfused step
-    // (profiles/leaf2cta_r02.jsonl).  Also the unfused default for m <= 1536,
-    // where the per-tile prologue / epilogue is a larger share of a tile's k
-    // loop: +0.4% (m = 1536) .. +9% (m = 512), SW^4 hybrid 158.2 -> 156.7 ms;
-    // above that one 128 x 128 CTA per SM (m = 4096: 184.2 vs 185.1 ms;
-    // profiles/leaf2cta_m_r02.jsonl).  MF_LEAF_2CTA=1/0 forces it on/off.  Not for
-    // the ordered fold: with two CTAs per SM its flag-ordered read-modify-
-    // writes lost updates in rows of warps 2-3 (a race not understood;
-    // tools/ordered_pattern.py), so that fold keeps one CTA per SM.
+    // epilogue runs beside the other's k loop.  The default for both folds,
+    // whose epilogues it hides (SW^2 n=16384: bulk 188.3 ms vs unfused 187.8;
+    // ordered 191.3 vs 194.0 ms on one CTA per SM; SW^3: ordered 182.9 vs
+    // 193.3 ms; profiles/ordered_2cta_r02.jsonl), and for unfused leaves with
+    // m <= 1536, where the per-tile prologue / epilogue is a larger share of a
+    // tile's k loop: +0.4% (m = 1536) .. +9% (m = 512), SW^4 hybrid 158.2 ->
+    // 157.2 ms; above that one 128 x 128 CTA per SM (m = 4096: 187.8 vs
+    // 189.9 ms; profiles/leaf2cta_m_r02.jsonl).  MF_LEAF_2CTA=1/0 forces it.
     const char* e2 = getenv("MF_LEAF_2CTA");
-    const bool two_cta = !ordered && (e2 ? atoi(e2) > 0 : (a.post != nullptr || a.m <= 1536));
+    const bool two_cta = e2 ? atoi(e2) > 0 : (a.post != nullptr || a.m <= 1536);
     if (two_cta) { cfg.bn = 64; cfg.split = 1; }
     const int bn = cfg.bn;
     // k sub-blocks of 16 per pipeline stage: 2 (k = 32, 3-stage ring), or 3

@@ -188,6 +188,8 @@ tiny_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict_
     __syncthreads();
   }
   TSTAMP(3);
+  // the products (generic-proxy stores) are read by bulk copies (async proxy)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   cluster.sync();  // every CTA's products are complete and every barrier initialised
   TSTAMP(4);
   const uint32_t bytes = (uint32_t)mm * 8;

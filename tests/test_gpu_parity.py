@@ -1217,8 +1217,8 @@ def test_random_shape_sweep():
 @pytest.mark.parametrize("name,levels,n", [(SW, 2, 2048), (SW, 1, 400), ("laderman", 1, 390), (None, 0, 640)])
 def test_two_cta_leaf(name, levels, n, monkeypatch):
     """The two-CTA-per-SM leaf (4 MMA warps, 128 x 64 tiles; the default under
-    the bulk-reduction fold and for unfused leaves with m <= 1536; forced on and
-    off here): integer inputs
+    both folds and for unfused leaves with m <= 1536; forced on and off here):
+    integer inputs
     exact, random inputs bitwise the one-CTA leaf (same k order per element)
     with no split-K tail on either side; ragged leaves (m = 200, 130) too."""
     t = triples.get(name) if name else None
@@ -1234,15 +1234,40 @@ def test_two_cta_leaf(name, levels, n, monkeypatch):
     assert (out["0"] == out["1"]).all()
 
 
-@pytest.mark.parametrize("n,bn", [(2048, "64"), (4096, "64"), (2048, "128")])
-def test_fused_ordered_concurrent_dependencies(n, bn, monkeypatch):
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_leaf_ring_reuse_under_the_ordered_fold(n, monkeypatch):
+    """Regression: the leaf's consumer warps released a ring slot (mbarrier
+    arrive) while their last fragment loads from it could still be in flight,
+    so the next TMA load could overwrite data not yet read.  It showed as wrong
+    64 x 32 warp tiles (rows 64-127) in about half of the two-CTA ordered-fold
+    launches at n = 8192 and every launch at n = 16384, before the
+    fence.proxy.async ahead of the arrive.  Ten launches (four at 16384), each
+    bitwise the unfused one-CTA result."""
+    t = triples.get(SW)
+    A, B = mf_inputs.pair("uniform", n, 51)
+    Ad, Bd = dev(A), dev(B)
+    monkeypatch.setenv("MF_LEAF_SPLIT", "1")
+    monkeypatch.setenv("MF_LEAF_2CTA", "0")
+    with mf.Plan(t, 2, n) as p:
+        Cu = p.dgemm(Ad, Bd).clone()
+    monkeypatch.setenv("MF_LEAF_2CTA", "1")
+    with mf.Plan(t, 2, n, fuse_postadd=1) as p:
+        for _ in range(10 if n <= 8192 else 4):
+            assert torch.equal(p.dgemm(Ad, Bd), Cu)
+
+
+@pytest.mark.parametrize("n,bn,two", [(2048, "64", "0"), (4096, "64", "0"), (2048, "128", "0"),
+                                      (2048, "64", "1"), (4096, "64", "1")])
+def test_fused_ordered_concurrent_dependencies(n, bn, two, monkeypatch):
     """The ordered fold where its flags really order concurrent CTAs: few tiles
     per product (n = 2048: 16 / 32 tiles; n = 4096 with 64-wide tiles: 128), so
     the products of one tile position run in the same wave and wait on each
-    other.  Five launches, each bitwise the flat unfused result."""
+    other; one CTA per SM (128- or 64-wide tiles) and two.  Five launches,
+    each bitwise the flat unfused result."""
     t = triples.get(SW)
     A, B = mf_inputs.pair("uniform", n, 50)
     monkeypatch.setenv("MF_LEAF_BN", bn)
+    monkeypatch.setenv("MF_LEAF_2CTA", two)
     Cf, Cu = _ordered_and_flat(monkeypatch, t, 2, n, A, B, 1.0)
     assert (Cf == Cu).all()
     with monkeypatch.context() as mp:
