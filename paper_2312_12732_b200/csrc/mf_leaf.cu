@@ -187,12 +187,11 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 }
 
 // Loads of C in the ordered fold: plain (weak) global loads after the flag's
-// ld.acquire -- the pattern the PTX memory model orders (the acquire
-// invalidates the SM's L1, so no stale line survives).  Measured: with two
-// CTAs per SM, ld.global.cg loads here returned data older than a co-resident
-// writer's released stores (rows of the other CTA's warps 2-3 lost updates),
-// weak loads did not.  "memory": must not move above the barrier that follows
-// the wait.
+// ld.acquire and a barrier -- the pattern the PTX memory model orders (the
+// acquire is followed by CCTL.IVALL: no stale L1 line survives).  "memory":
+// must not move above the barrier that follows the wait.  (Wrong tiles once
+// blamed on these loads were the k loop's ring-release race; see the fence
+// before mbar_arrive.)
 __device__ __forceinline__ void ld_v2(const double* p, double& x, double& y) {
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "l"(p) : "memory");
 }
