@@ -831,10 +831,16 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     // 193.3 ms; profiles/ordered_2cta_r02.jsonl), and for unfused leaves with
     // m <= 1536, where the per-tile prologue / epilogue is a larger share of a
     // tile's k loop: +0.4% (m = 1536) .. +9% (m = 512), SW^4 hybrid 158.2 ->
-    // 157.2 ms; above that one 128 x 128 CTA per SM (m = 4096: 187.8 vs
-    // 189.9 ms; profiles/leaf2cta_m_r02.jsonl).  MF_LEAF_2CTA=1/0 forces it.
+    // 157.2 ms -- when its 128 x 64 tiles fill at least one wave of two CTAs
+    // per SM (smaller grids keep one CTA per SM and its split-K tail: n = 1024
+    // SW^1, 224 tiles: 0.114 vs 0.118 ms); above m = 1536 one 128 x 128 CTA per
+    // SM (m = 4096: 187.8 vs 189.9 ms; profiles/leaf2cta_m_r02.jsonl).
+    // MF_LEAF_2CTA=1/0 forces it.
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles64 = tm_tiles * ((c1 - c0 + 63) / 64) * a.n_jobs;
     const char* e2 = getenv("MF_LEAF_2CTA");
-    const bool two_cta = e2 ? atoi(e2) > 0 : (a.post != nullptr || a.m <= 1536);
+    const bool two_cta = e2 ? atoi(e2) > 0 : (a.post != nullptr || (a.m <= 1536 && tiles64 >= 2 * sms));
     if (two_cta) { cfg.bn = 64; cfg.split = 1; }
     const int bn = cfg.bn;
     // k sub-blocks of 16 per pipeline stage: 2 (k = 32, 3-stage ring), or 3
