@@ -851,6 +851,10 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (ksub == 3 && bn != 128) ksub = 2;
     const bool fuse = a.post != nullptr;
     if (fuse) ksub = 2;  // the fused tile is staged in the KSUB=2 ring
+    // the two-CTA shape has only the KSUB = 2 instantiation (KSUB = 1 with 4
+    // stages measured 1.1% slower at n=16384 SW^2); set before the B box and
+    // kblocks below are derived from ksub
+    if (two_cta) ksub = 2;
     if (ordered &&
         (int64_t)a.P * a.P * ((r1 - r0 + BM - 1) / BM) * ((c1 - c0 + bn - 1) / bn) > a.fuse_sync_len)
       return cudaErrorInvalidValue;
@@ -889,7 +893,6 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     // the >48 KB dynamic shared memory opt-in is per device: once per
     // (device, instantiation)
-    if (two_cta) ksub = 2;  // (KSUB = 1 with 4 stages measured 1.1% slower at n=16384 SW^2)
     static std::atomic<uint64_t> attr_set[12];
     const int inst = two_cta ? (ordered ? 10 : fuse ? 11 : 9)
                      : ordered ? (bn == 64 ? 8 : 7)

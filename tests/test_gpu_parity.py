@@ -1234,6 +1234,20 @@ def test_two_cta_leaf(name, levels, n, monkeypatch):
     assert (out["0"] == out["1"]).all()
 
 
+@pytest.mark.parametrize("ksub", ["1", "2", "3"])
+@pytest.mark.parametrize("two", ["0", "1"])
+def test_leaf_ksub_override_on_both_shapes(ksub, two, monkeypatch):
+    """MF_LEAF_KSUB (k sub-blocks per ring stage) on the one- and two-CTA leaf:
+    the two-CTA shape has only KSUB = 2 and must build its B box and k-block
+    count from that, whatever the override (m = 512, 1536: integers exact)."""
+    monkeypatch.setenv("MF_LEAF_KSUB", ksub)
+    monkeypatch.setenv("MF_LEAF_2CTA", two)
+    for n in (2048, 3072):
+        A, B = mf_inputs.pair("int1024", n, 52)
+        with mf.Plan(triples.get(SW), 2, n) as p:
+            assert (host(p.dgemm(dev(A), dev(B))) == exact(A, B)).all(), (n, ksub, two)
+
+
 @pytest.mark.parametrize("n", [8192, 16384])
 def test_leaf_ring_reuse_under_the_ordered_fold(n, monkeypatch):
     """Regression: the leaf's consumer warps released a ring slot (mbarrier
