@@ -880,7 +880,6 @@ cudaError_t launch_leaf(const LeafArgs& a, int leaf_kind, cudaStream_t s) {
     prm.post_off = a.post_off;
     prm.post = a.post;
     prm.sync = a.fuse_sync;
-    // prefetch the C tiles ~8 stages (256 k) before the end of the k loop
     prm.nP = a.P;
     prm.split = cfg.split;
     prm.n_whole = cfg.split > 1 ? (int)cfg.n_whole : 0;
